@@ -1,0 +1,205 @@
+/* bbtc.h — C-ABI of the B200-native block-based triangle counter (BBTC).
+ *
+ * Method: Yaşar, Rajamanickam, Berry, Çatalyürek, "A Block-Based Triangle
+ * Counting Algorithm on Heterogeneous Environments" (arXiv 2009.12457).
+ * Citations "P:n" are lines of that paper's text.
+ *
+ * Pipeline (every step runs in this library's sm_100a kernels, on the device):
+ *   bbtc_graph_from_edges  a1-a2  canonicalise the raw edge list, full
+ *                                 degrees, stable degree rank, orient each
+ *                                 edge from lower to higher rank
+ *   bbtc_plan_create       a3-a5  symmetric rectilinear cut vector,
+ *                                 the p(p+1)/2 upper blocks G_ij as block CSR (BCSR,
+ *                                 P:460-463, Fig. 2d), the task list of Alg. 4
+ *   bbtc_count             a7-a8  for every task t=(i,j,k): for every edge (u,v) in G_ij,
+ *                                 |N(G_ik,u) ∩ N(G_jk,v)| (Alg. 5), summed per
+ *                                 task into uint64 counters
+ *   bbtc_plan_to_host / bbtc_stage / BBTC_COUNT_STREAM   a6  blocks kept in pinned host
+ *                                 memory and streamed host->device in task order with
+ *                                 copy/compute overlap (Alg. 7 asyncCopy)
+ *
+ * Conventions (all calls):
+ *   - Return bbtc_status: 0 = OK, < 0 = error; bbtc_last_error() gives a message
+ *     for the calling thread's last error (valid until its next call).
+ *   - Vertex ids are uint32 (id 0xFFFFFFFF is rejected with BBTC_ERANGE); edge
+ *     counts and global offsets are uint64; counts are uint64 (Friendster has
+ *     4.17e9 triangles).
+ *   - "host" pointers are ordinary (or pinned) CPU memory; "device" pointers are
+ *     CUDA global memory on the context's device.  Inputs are borrowed for the
+ *     duration of the call only (copied or consumed before return, except
+ *     *_async calls which consume them in stream order).  Outputs are
+ *     caller-allocated; size them from bbtc_graph_stats / bbtc_plan_info.
+ *   - Handles (bbtc_ctx, bbtc_graph, bbtc_plan) are library-owned until *_free.
+ *     A plan does not reference its graph after bbtc_plan_create returns.
+ *   - Threading: a context serialises its work on one CUDA stream; use one
+ *     context per host thread.  Graphs and plans are immutable after creation.
+ *   - The library never falls back to a CPU path: with no usable CUDA device,
+ *     bbtc_ctx_create fails with BBTC_ECUDA.
+ */
+#ifndef BBTC_H
+#define BBTC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBTC_API __attribute__((visibility("default")))
+
+typedef enum {
+  BBTC_OK = 0,
+  BBTC_EINVAL = -1,   /* bad argument (NULL handle, invalid cuts, p == 0 with no budget …) */
+  BBTC_ENOMEM = -2,   /* device or host allocation failed */
+  BBTC_EIO = -3,      /* reserved (file input) */
+  BBTC_EPARSE = -4,   /* reserved (file input) */
+  BBTC_ERANGE = -5,   /* a size does not fit the documented index widths */
+  BBTC_ECUDA = -6,    /* CUDA runtime error (message carries cudaGetErrorString) */
+  BBTC_ENCCL = -7,    /* reserved (collectives run in the caller's process group) */
+  BBTC_ESTATE = -8    /* call not valid in the object's current state */
+} bbtc_status;
+
+typedef struct bbtc_ctx bbtc_ctx;
+typedef struct bbtc_graph bbtc_graph;
+typedef struct bbtc_plan bbtc_plan;
+
+/* ---------------------------------------------------------------- context */
+typedef struct {
+  int device;            /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t to enqueue on; NULL = library-created stream */
+  uint32_t copy_streams; /* streams used for host->device block copies (0 = default 2) */
+  uint32_t reserved;
+} bbtc_ctx_opts;
+
+/* Creates a context on opts->device (opts may be NULL: device 0, own stream).
+ * Errors: BBTC_ECUDA if the device is unavailable. */
+BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out);
+BBTC_API void bbtc_ctx_free(bbtc_ctx* ctx);
+/* Blocks until all work enqueued on the context has finished. */
+BBTC_API bbtc_status bbtc_ctx_sync(bbtc_ctx* ctx);
+
+/* ------------------------------------------------------------------ graph */
+#define BBTC_MEM_HOST 0
+#define BBTC_MEM_DEVICE 1
+
+typedef struct {
+  uint32_t n;               /* vertices: max(n_hint, 1 + largest id in the raw input) */
+  uint32_t n_nonisolated;   /* vertices with degree > 0 */
+  uint64_t m;               /* unique undirected edges after canonicalisation */
+  uint64_t raw_edges;       /* input pairs (incl. self-loops / duplicates) */
+  uint32_t d_max;           /* largest full degree d(G,u) in the undirected graph */
+  uint32_t reserved;
+} bbtc_graph_stats;
+
+/* a1-a2.  src/dst: n_edges raw pairs (uint32 each), in host memory (mem ==
+ * BBTC_MEM_HOST; copied host->device in chunks overlapped with the first kernel;
+ * pinned memory is fastest) or device memory (mem == BBTC_MEM_DEVICE).  The raw
+ * list may hold self-loops (dropped), duplicates and both orientations (merged),
+ * P:222-228.  The degree rank sorts vertices by (full degree ascending, input id
+ * ascending) — the paper leaves ties open; this fixes them.
+ * Errors: BBTC_EINVAL (NULL pointers with n_edges > 0), BBTC_ERANGE (an id ==
+ * 0xFFFFFFFF, or m >= 2^32-1), BBTC_ENOMEM, BBTC_ECUDA. */
+BBTC_API bbtc_status bbtc_graph_from_edges(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst,
+                                           uint64_t n_edges, uint32_t n_hint, int mem, bbtc_graph** out);
+BBTC_API bbtc_status bbtc_graph_stats_get(const bbtc_graph* g, bbtc_graph_stats* s);
+/* rank_of_input_id: host, n entries. */
+BBTC_API bbtc_status bbtc_graph_rank(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t* rank_of_input_id);
+/* The oriented graph in rank space as CSR (row_ptr host n+1, col host m); rows
+ * sorted ascending.  For tests and inspection (it sorts on demand). */
+BBTC_API bbtc_status bbtc_graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col);
+BBTC_API void bbtc_graph_free(bbtc_graph* g);
+
+/* ------------------------------------------------------------------- plan */
+typedef struct {
+  uint32_t p;               /* parts after clamping (p > n -> n; n == 0 -> 1) */
+  uint32_t clamped;         /* 1 if the requested p was clamped */
+  uint64_t n_tasks;         /* p(p+1)(p+2)/6 */
+  uint64_t n_blocks;        /* p(p+1)/2 upper-triangular blocks */
+  uint64_t m;               /* edges (sum of block nnz) */
+  uint64_t m_max;           /* largest block nnz */
+  double lambda;            /* load imbalance m_max / m_avg, m_avg = 2m/(p(p+1)) */
+  uint32_t dmax_blk;        /* d'_max: largest partial degree d(G_ij,u) over all blocks */
+  uint32_t host_blocks;     /* 1 if the blocks live in pinned host memory (bbtc_plan_to_host) */
+  uint64_t block_bytes;     /* bytes of all blocks (row offsets + cols + row ids) */
+  uint64_t max_task_bytes;  /* largest 3-block footprint of one task */
+  uint64_t b_alg;           /* algorithmic bytes of the count, 0 unless
+                               BBTC_PLAN_STATS was passed */
+  uint64_t visits;          /* edge visits summed over tasks, i.e. sum_t nnz(G_ij); ditto */
+  uint64_t work_items;      /* work items the count kernel schedules */
+} bbtc_plan_info;
+
+#define BBTC_PLAN_STATS 1u   /* compute b_alg / visits / dmax_blk (one extra device pass) */
+
+/* a3-a5.  p: requested parts (>= 1; clamped to n).  cuts: NULL for the default
+ * rule (R5: full-degree prefix rule) or a host array of p+1 entries
+ * with cuts[0] = 0, cuts[p] = n, non-decreasing (empty parts allowed).
+ * When cuts is given, p must equal its length - 1 and is not clamped.
+ * Block (i,j), i <= j, holds the edges (u,v) with u in V_i, v in V_j
+ * as BCSR: row offsets uint32[|V_i|+1] over local row ids u - cuts[i], column ids
+ * uint32 v - cuts[j] (rows ascending), plus the local row id of every edge.
+ * Errors: BBTC_EINVAL (p == 0, bad cuts), BBTC_ERANGE (2*ceil(log2 n) +
+ * ceil(log2 p) > 64 bits of sort key), BBTC_ENOMEM, BBTC_ECUDA. */
+BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                      uint32_t flags, bbtc_plan** out);
+BBTC_API bbtc_status bbtc_plan_info_get(const bbtc_plan* plan, bbtc_plan_info* info);
+/* cuts: host, p+1 entries. */
+BBTC_API bbtc_status bbtc_plan_cuts(const bbtc_plan* plan, uint32_t* cuts);
+/* Copies block (i,j) to host: row_ptr (|V_i|+1), col (nnz), row (nnz); any may
+ * be NULL.  *nnz receives the block's edge count.  Errors: BBTC_EINVAL (i > j). */
+BBTC_API bbtc_status bbtc_plan_block(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t i, uint32_t j,
+                                     uint32_t* row_ptr, uint32_t* col, uint32_t* row, uint64_t* nnz);
+/* a6: moves the blocks into pinned host memory and releases their device copy
+ * (the out-of-core form of the plan).  bbtc_count then streams them. */
+BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan);
+BBTC_API void bbtc_plan_free(bbtc_plan* plan);
+
+/* Task numbering (Alg. 4): tasks i <= j <= k in loop order.
+ * idx(i,j,k) = [C(p+2,3) - C(p-i+2,3)] + [C(p-i+1,2) - C(p-j+1,2)] + (k-j). */
+BBTC_API uint64_t bbtc_n_tasks(uint32_t p);
+BBTC_API bbtc_status bbtc_task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k, uint64_t* idx);
+BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32_t* j, uint32_t* k);
+
+/* ------------------------------------------------------------------ count */
+typedef struct {
+  double t_total_ms;   /* host wall time of the call */
+  double t_h2d_ms;     /* time the copy streams were busy (streamed plans) */
+  double t_kernel_ms;  /* device time of the count kernel(s) (CUDA events) */
+  uint64_t h2d_bytes;  /* block bytes copied host->device by this call */
+  uint64_t launches;   /* kernels launched by this call */
+} bbtc_timing;
+
+#define BBTC_COUNT_DEFAULT 0u
+
+/* a7-a8, asynchronous.  Enqueues the count of this rank's share of the work on
+ * the context stream and returns.  d_counts: DEVICE uint64[n_tasks + 1]; it is
+ * zeroed, then d_counts[t] receives the triangles of task t (Alg. 4 order) found
+ * by this rank and d_counts[n_tasks] their sum.  rank/world split the work
+ * items statically (rank r takes items r, r+world, … in the plan's balanced
+ * order); summing d_counts over ranks (one all-reduce) gives the full result.
+ * world = 1, rank = 0 counts everything.  Requires device-resident blocks
+ * (plans made by bbtc_plan_create, or bbtc_stage after bbtc_plan_to_host).
+ * Errors: BBTC_EINVAL, BBTC_ESTATE (blocks not resident), BBTC_ECUDA. */
+BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
+                                      uint64_t* d_counts);
+
+/* a6-a8, synchronous.  Like bbtc_count_async but returns results in HOST
+ * memory: *total and (if per_task != NULL) per_task[n_tasks].  Blocks that are
+ * in pinned host memory and not resident are streamed host->device on the copy
+ * streams, overlapped with the kernels of earlier tasks.  t may be NULL. */
+BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
+                                uint32_t flags, uint64_t* total, uint64_t* per_task, bbtc_timing* t);
+
+/* a6: makes every block of a host-resident plan resident on the context's
+ * device (so a following count runs "excl. H2D").  No-op for device plans. */
+BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan);
+/* Drops the device copies made by bbtc_stage / streaming counts. */
+BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan);
+
+/* Number of kernels this library launched on the context since creation. */
+BBTC_API uint64_t bbtc_ctx_launches(const bbtc_ctx* ctx);
+BBTC_API const char* bbtc_last_error(void);
+BBTC_API const char* bbtc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,219 @@
+"""bbtc-b200: B200-native block-based triangle counting (BBTC, arXiv 2009.12457).
+
+Thin Python layer over libbbtc.so (include/bbtc.h).  The classes only marshal
+arguments and own handles; every step of the path (canonicalise, degree order,
+partition, BCSR, count) runs in the library's sm_100a kernels.
+
+    ctx   = Context(device=0)
+    g     = Graph.from_edges(ctx, src, dst, n_hint)   # numpy (host) or torch CUDA tensors
+    plan  = Plan(ctx, g, p=16)                       # cuts, blocks, tasks (Alg. 4)
+    total, per_task = plan.count()                   # uint64 total + per-task (Alg. 4 order)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import BBTCError, MEM_DEVICE, MEM_HOST, PLAN_STATS
+
+__all__ = ["Context", "Graph", "Plan", "BBTCError", "n_tasks", "task_index", "task_ijk", "count_triangles"]
+
+
+def _ptr(x, want_dtype):
+    """(pointer, length, mem) of a host numpy array or a CUDA tensor."""
+    if hasattr(x, "data_ptr") and hasattr(x, "is_cuda"):
+        import torch
+        assert x.is_contiguous(), "tensor must be contiguous"
+        assert x.dtype in (torch.int32, torch.uint32), "edge arrays must be 32-bit"
+        return ctypes.c_void_p(x.data_ptr()), x.numel(), (MEM_DEVICE if x.is_cuda else MEM_HOST)
+    a = np.ascontiguousarray(x, dtype=want_dtype)
+    return ctypes.c_void_p(a.ctypes.data), len(a), MEM_HOST, a
+
+
+def n_tasks(p: int) -> int:
+    return int(L.bbtc_n_tasks(p))
+
+
+def task_index(p: int, i: int, j: int, k: int) -> int:
+    out = ctypes.c_uint64()
+    L.check(L.bbtc_task_index(p, i, j, k, ctypes.byref(out)))
+    return int(out.value)
+
+
+def task_ijk(p: int, idx: int):
+    i, j, k = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+    L.check(L.bbtc_task_ijk(p, idx, ctypes.byref(i), ctypes.byref(j), ctypes.byref(k)))
+    return int(i.value), int(j.value), int(k.value)
+
+
+class Context:
+    """A CUDA device + the stream the library enqueues on (bbtc_ctx)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None, copy_streams: int = 0):
+        o = L.bbtc_ctx_opts(device, ctypes.c_void_p(stream) if stream else None, copy_streams, 0)
+        h = ctypes.c_void_p()
+        L.check(L.bbtc_ctx_create(ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sync(self):
+        L.check(L.bbtc_ctx_sync(self._h))
+
+    @property
+    def launches(self) -> int:
+        return int(L.bbtc_ctx_launches(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.bbtc_ctx_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Graph:
+    """Canonical, degree-ranked, oriented graph on the device (bbtc_graph)."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx = ctx
+        self._h = h
+
+    @classmethod
+    def from_edges(cls, ctx: Context, src, dst, n_hint: int = 0) -> "Graph":
+        ps = _ptr(src, np.uint32)
+        pd = _ptr(dst, np.uint32)
+        assert ps[1] == pd[1], "src and dst differ in length"
+        assert ps[2] == pd[2], "src and dst must both be host or both device"
+        h = ctypes.c_void_p()
+        L.check(L.bbtc_graph_from_edges(ctx.handle, ps[0], pd[0], ps[1], n_hint, ps[2], ctypes.byref(h)))
+        return cls(ctx, h)
+
+    def stats(self) -> dict:
+        s = L.bbtc_graph_stats()
+        L.check(L.bbtc_graph_stats_get(self._h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_ if f != "reserved"}
+
+    @property
+    def n(self) -> int:
+        return self.stats()["n"]
+
+    @property
+    def m(self) -> int:
+        return self.stats()["m"]
+
+    def rank(self) -> np.ndarray:
+        r = np.empty(self.n, np.uint32)
+        L.check(L.bbtc_graph_rank(self.ctx.handle, self._h, r.ctypes.data_as(L._u32p)))
+        return r
+
+    def csr(self):
+        st = self.stats()
+        row = np.empty(st["n"] + 1, np.uint64)
+        col = np.empty(st["m"], np.uint32)
+        L.check(L.bbtc_graph_csr(self.ctx.handle, self._h, row.ctypes.data_as(L._u64p), col.ctypes.data_as(L._u32p)))
+        return row, col
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.bbtc_graph_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Plan:
+    """Cut vector + BCSR blocks + task list (bbtc_plan)."""
+
+    def __init__(self, ctx: Context, graph: Graph, p: int = 1, cuts=None, stats: bool = False):
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        cptr = None
+        if cuts is not None:
+            self._cuts_in = np.ascontiguousarray(cuts, dtype=np.uint32)
+            p = len(self._cuts_in) - 1
+            cptr = self._cuts_in.ctypes.data_as(L._u32p)
+        L.check(L.bbtc_plan_create(ctx.handle, graph._h, p, cptr, PLAN_STATS if stats else 0, ctypes.byref(h)))
+        self._h = h
+
+    def info(self) -> dict:
+        i = L.bbtc_plan_info()
+        L.check(L.bbtc_plan_info_get(self._h, ctypes.byref(i)))
+        d = {f: getattr(i, f) for f, _ in i._fields_}
+        d["lambda"] = d.pop("lambda_")
+        return d
+
+    @property
+    def p(self) -> int:
+        return self.info()["p"]
+
+    @property
+    def n_tasks(self) -> int:
+        return self.info()["n_tasks"]
+
+    def cuts(self) -> np.ndarray:
+        c = np.empty(self.p + 1, np.uint32)
+        L.check(L.bbtc_plan_cuts(self._h, c.ctypes.data_as(L._u32p)))
+        return c
+
+    def block(self, i: int, j: int):
+        """(row_ptr, col, row) of block G_ij with block-local ids."""
+        nnz = ctypes.c_uint64()
+        L.check(L.bbtc_plan_block(self.ctx.handle, self._h, i, j, None, None, None, ctypes.byref(nnz)))
+        c = self.cuts()
+        rp = np.empty(int(c[i + 1] - c[i]) + 1, np.uint32)
+        col = np.empty(nnz.value, np.uint32)
+        row = np.empty(nnz.value, np.uint32)
+        L.check(L.bbtc_plan_block(self.ctx.handle, self._h, i, j, rp.ctypes.data_as(L._u32p),
+                                  col.ctypes.data_as(L._u32p), row.ctypes.data_as(L._u32p), None))
+        return rp, col, row
+
+    def to_host(self):
+        L.check(L.bbtc_plan_to_host(self.ctx.handle, self._h))
+
+    def stage(self):
+        L.check(L.bbtc_stage(self.ctx.handle, self._h))
+
+    def unstage(self):
+        L.check(L.bbtc_unstage(self.ctx.handle, self._h))
+
+    def count(self, rank: int = 0, world: int = 1, timing: bool = False):
+        """Synchronous count: (total, per_task uint64[n_tasks] in Alg. 4 order[, timing dict])."""
+        tot = ctypes.c_uint64()
+        pt = np.zeros(self.n_tasks, np.uint64)
+        tm = L.bbtc_timing()
+        L.check(L.bbtc_count(self.ctx.handle, self._h, rank, world, 0, ctypes.byref(tot),
+                             pt.ctypes.data_as(L._u64p), ctypes.byref(tm)))
+        if timing:
+            return int(tot.value), pt, {f: getattr(tm, f) for f, _ in tm._fields_}
+        return int(tot.value), pt
+
+    def count_async(self, d_counts, rank: int = 0, world: int = 1):
+        """Enqueue the count into a CUDA uint64/int64 tensor of n_tasks+1 entries (last = total)."""
+        assert d_counts.is_cuda and d_counts.numel() >= self.n_tasks + 1 and d_counts.element_size() == 8
+        L.check(L.bbtc_count_async(self.ctx.handle, self._h, rank, world, ctypes.c_void_p(d_counts.data_ptr())))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.bbtc_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def count_triangles(src, dst, n_hint: int = 0, p: int = 1, cuts=None, device: int = 0, ctx: Context | None = None):
+    """One-shot: returns dict(total, per_task, cuts, n, m)."""
+    ctx = ctx or Context(device)
+    g = Graph.from_edges(ctx, src, dst, n_hint)
+    plan = Plan(ctx, g, p, cuts)
+    tot, pt = plan.count()
+    st = g.stats()
+    return dict(total=tot, per_task=pt, cuts=plan.cuts(), n=st["n"], m=st["m"], plan=plan, graph=g)

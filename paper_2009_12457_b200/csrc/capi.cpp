@@ -1,0 +1,496 @@
+// capi.cpp — the extern "C" surface of libbbtc (include/bbtc.h) and its host runtime:
+// error mapping, contexts, task enumeration (Alg. 4), work items, the block
+// streamer (a6) and the synchronous count driver (Alg. 9's role).
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+#include "internal.h"
+
+namespace bbtc {
+
+static thread_local std::string t_err;
+void set_error(const std::string& msg) { t_err = msg; }
+[[noreturn]] void raise(bbtc_status code, const std::string& msg) { throw Error{code, msg}; }
+
+template <class F>
+static bbtc_status guard(F f) {
+  try {
+    f();
+    return BBTC_OK;
+  } catch (const Error& e) {
+    t_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_err = "host allocation failed";
+    return BBTC_ENOMEM;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return BBTC_EINVAL;
+  }
+}
+
+static inline uint64_t C2(uint64_t n) { return n < 2 ? 0 : n * (n - 1) / 2; }
+static inline uint64_t C3(uint64_t n) { return n < 3 ? 0 : n * (n - 1) * (n - 2) / 6; }
+
+uint64_t n_tasks(uint32_t p) { return (uint64_t)p * (p + 1) * (p + 2) / 6; }
+
+// Closed form of the Alg. 4 position (tasks with first index < i, then second index
+// < j within i, then k - j): [C(p+2,3) - C(p-i+2,3)] + [C(p-i+1,2) - C(p-j+1,2)] + (k-j).
+uint64_t task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k) {
+  return (C3((uint64_t)p + 2) - C3((uint64_t)p - i + 2)) + (C2((uint64_t)p - i + 1) - C2((uint64_t)p - j + 1)) +
+         (k - j);
+}
+
+// Tasks in execution order + work items.  Execution order groups tasks sharing the
+// randomly gathered block G_jk (for k: for j <= k: for i <= j), so consecutive work
+// items keep G_jk and G_ik L2-resident.  Each task's G_ij edges are cut into items
+// of `chunk` edges (the unit a warp claims).
+void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
+  const uint32_t p = plan->p;
+  plan->tasks.clear();
+  plan->tasks.reserve(n_tasks(p));
+  // Chunk: enough items for ~16 per warp slot on 148 SMs, within [256, 4096].
+  const uint64_t visits_est = [&] {
+    uint64_t v = 0;
+    for (uint32_t j = 0; j < p; ++j)
+      for (uint32_t i = 0; i <= j; ++i) v += plan->blocks[block_id(i, j)].nnz * (p - j);
+    return v;
+  }();
+  uint64_t chunk = visits_est / (148ull * 64 * 16);
+  chunk = std::max<uint64_t>(256, std::min<uint64_t>(4096, (chunk + 31) / 32 * 32));
+  plan->chunk = (uint32_t)chunk;
+  plan->item_start.assign(1, 0);
+  uint64_t max_task_bytes = 0;
+  auto bbytes = [&](uint32_t b) {
+    const BlockDesc& B = plan->blocks[b];
+    return 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+  };
+  for (uint32_t k = 0; k < p; ++k)
+    for (uint32_t j = 0; j <= k; ++j)
+      for (uint32_t i = 0; i <= j; ++i) {
+        TaskDesc T;
+        T.ij = block_id(i, j);
+        T.ik = block_id(i, k);
+        T.jk = block_id(j, k);
+        T.idx = (uint32_t)task_index(p, i, j, k);
+        plan->tasks.push_back(T);
+        const uint64_t nnz = plan->blocks[T.ij].nnz;
+        plan->item_start.push_back(plan->item_start.back() + (nnz + chunk - 1) / chunk);
+        uint64_t tb = bbytes(T.ij) + (T.ik != T.ij ? bbytes(T.ik) : 0) +
+                      (T.jk != T.ij && T.jk != T.ik ? bbytes(T.jk) : 0);
+        max_task_bytes = std::max(max_task_bytes, tb);
+      }
+  plan->info.work_items = plan->item_start.back();
+  plan->info.max_task_bytes = max_task_bytes;
+  bbtc_ctx* ctx = plan->ctx;
+  plan->d_tasks.alloc(plan->tasks.size(), ctx->stream);
+  plan->d_item_start.alloc(plan->item_start.size(), ctx->stream);
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_tasks.p, plan->tasks.data(), plan->tasks.size() * sizeof(TaskDesc),
+                            cudaMemcpyHostToDevice, ctx->stream));
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_item_start.p, plan->item_start.data(), plan->item_start.size() * 8,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  // The host vectors are read by the async copies above: make them complete
+  // before the caller can mutate the plan.
+  BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---- a6: the block streamer -------------------------------------------------------
+// A host-resident plan keeps its three arenas in pinned memory.  Streaming copies
+// every block the first time a task in execution order needs it (on the copy
+// streams, round-robin), and launches the count kernel over each maximal run of
+// tasks whose blocks have all been issued, after waiting on their copy events —
+// so block copies of later tasks overlap the kernels of earlier ones (Alg. 7's
+// prefetch of the next task's blocks).
+struct Streamer {
+  bbtc_ctx* ctx;
+  bbtc_plan* plan;
+  std::vector<char> issued;
+  std::vector<cudaEvent_t> ev;      // per block: copy finished
+  uint64_t bytes = 0;
+  uint32_t rr = 0;
+
+  Streamer(bbtc_ctx* c, bbtc_plan* p) : ctx(c), plan(p), issued(p->blocks.size(), 0), ev(p->blocks.size(), nullptr) {}
+  ~Streamer() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  uint64_t block_bytes(uint32_t b) const {
+    const BlockDesc& B = plan->blocks[b];
+    return 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+  }
+  void issue(uint32_t b) {
+    if (issued[b]) return;
+    issued[b] = 1;
+    const BlockDesc& B = plan->blocks[b];
+    cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
+    const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+    if (B.nnz) {
+      BBTC_CUDA(cudaMemcpyAsync(plan->cols.p + B.e0, plan->h_cols + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
+      BBTC_CUDA(cudaMemcpyAsync(plan->rows.p + B.e0, plan->h_rows + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
+    }
+    BBTC_CUDA(cudaMemcpyAsync(plan->rowptr.p + B.ro, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
+    BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    BBTC_CUDA(cudaEventRecord(ev[b], cs));
+    bytes += block_bytes(b);
+  }
+};
+
+static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (plan->cols.p || plan->m == 0) {
+    if (!plan->rowptr.p) {
+      uint64_t ro = 0;
+      for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+      plan->rowptr.alloc(ro, ctx->stream);
+    }
+    return;
+  }
+  uint64_t ro = 0;
+  for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+  plan->cols.alloc(plan->m, ctx->stream);
+  plan->rows.alloc(plan->m, ctx->stream);
+  plan->rowptr.alloc(ro, ctx->stream);
+}
+
+static uint64_t rowptr_len(const bbtc_plan* plan) {
+  uint64_t ro = 0;
+  for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+  return ro;
+}
+
+}  // namespace bbtc
+
+using namespace bbtc;
+
+extern "C" {
+
+BBTC_API const char* bbtc_last_error(void) { return t_err.c_str(); }
+BBTC_API const char* bbtc_version(void) { return "bbtc-b200 0.1 (sm_100a)"; }
+
+BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out) {
+  return guard([&] {
+    if (!out) raise(BBTC_EINVAL, "out is NULL");
+    *out = nullptr;
+    bbtc_ctx_opts o{};
+    if (opts) o = *opts;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+      raise(BBTC_ECUDA, std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "count 0"));
+    if (o.device < 0 || o.device >= ndev) raise(BBTC_EINVAL, "device ordinal out of range");
+    BBTC_CUDA(cudaSetDevice(o.device));
+    int major = 0;
+    BBTC_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, o.device));
+    if (major != 10) raise(BBTC_ECUDA, "libbbtc is built for sm_100a (B200) only");
+    auto* c = new bbtc_ctx();
+    c->device = o.device;
+    BBTC_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, o.device));
+    if (o.stream) {
+      c->stream = (cudaStream_t)o.stream;
+    } else {
+      BBTC_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    const uint32_t ncs = o.copy_streams ? o.copy_streams : 2;
+    for (uint32_t x = 0; x < ncs; ++x) {
+      cudaStream_t s;
+      BBTC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      c->copy_streams.push_back(s);
+    }
+    // Keep freed pool memory cached between steps (no OS round trips per call).
+    cudaMemPool_t pool;
+    BBTC_CUDA(cudaDeviceGetDefaultMemPool(&pool, o.device));
+    uint64_t thr = ~0ull;
+    BBTC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = c;
+  });
+}
+
+BBTC_API void bbtc_ctx_free(bbtc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto s : c->copy_streams) cudaStreamDestroy(s);
+  if (c->cursor) cudaFree(c->cursor);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+BBTC_API bbtc_status bbtc_ctx_sync(bbtc_ctx* c) {
+  return guard([&] {
+    if (!c) raise(BBTC_EINVAL, "ctx is NULL");
+    BBTC_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+BBTC_API uint64_t bbtc_ctx_launches(const bbtc_ctx* c) { return c ? c->launches : 0; }
+
+BBTC_API bbtc_status bbtc_graph_from_edges(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t n_edges,
+                                           uint32_t n_hint, int mem, bbtc_graph** out) {
+  return guard([&] {
+    if (!ctx || !out) raise(BBTC_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+    if (n_edges && (!src || !dst)) raise(BBTC_EINVAL, "src/dst is NULL");
+    if (mem != BBTC_MEM_HOST && mem != BBTC_MEM_DEVICE) raise(BBTC_EINVAL, "mem must be BBTC_MEM_HOST or _DEVICE");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new bbtc_graph();
+    g->ctx = ctx;
+    try {
+      graph_build(ctx, src, dst, n_edges, n_hint, mem, g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+BBTC_API bbtc_status bbtc_graph_stats_get(const bbtc_graph* g, bbtc_graph_stats* s) {
+  return guard([&] {
+    if (!g || !s) raise(BBTC_EINVAL, "NULL argument");
+    s->n = g->n;
+    s->n_nonisolated = g->n_nonisolated;
+    s->m = g->m;
+    s->raw_edges = g->raw;
+    s->d_max = g->d_max;
+    s->reserved = 0;
+  });
+}
+
+BBTC_API bbtc_status bbtc_graph_rank(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t* rank) {
+  return guard([&] {
+    if (!ctx || !g || (!rank && g->n)) raise(BBTC_EINVAL, "NULL argument");
+    BBTC_CUDA(cudaMemcpyAsync(rank, g->rank.p, (size_t)g->n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+BBTC_API bbtc_status bbtc_graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col) {
+  return guard([&] {
+    if (!ctx || !g || !row_ptr || (!col && g->m)) raise(BBTC_EINVAL, "NULL argument");
+    graph_csr(ctx, g, row_ptr, col);
+  });
+}
+
+BBTC_API void bbtc_graph_free(bbtc_graph* g) { delete g; }
+
+BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                      uint32_t flags, bbtc_plan** out) {
+  return guard([&] {
+    if (!ctx || !g || !out) raise(BBTC_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (p == 0) raise(BBTC_EINVAL, "p must be >= 1");
+    if (cuts && p > 4096) raise(BBTC_ERANGE, "p > 4096");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    auto* plan = new bbtc_plan();
+    plan->ctx = ctx;
+    try {
+      plan_build(ctx, g, p, cuts, flags, plan);
+    } catch (...) {
+      delete plan;
+      throw;
+    }
+    *out = plan;
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_info_get(const bbtc_plan* plan, bbtc_plan_info* info) {
+  return guard([&] {
+    if (!plan || !info) raise(BBTC_EINVAL, "NULL argument");
+    *info = plan->info;
+    info->host_blocks = plan->host_blocks;
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_cuts(const bbtc_plan* plan, uint32_t* cuts) {
+  return guard([&] {
+    if (!plan || !cuts) raise(BBTC_EINVAL, "NULL argument");
+    std::copy(plan->cuts.begin(), plan->cuts.end(), cuts);
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_block(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t i, uint32_t j, uint32_t* row_ptr,
+                                     uint32_t* col, uint32_t* row, uint64_t* nnz) {
+  return guard([&] {
+    if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
+    if (i > j || j >= plan->p) raise(BBTC_EINVAL, "need i <= j < p");
+    const BlockDesc& B = plan->blocks[block_id(i, j)];
+    if (nnz) *nnz = B.nnz;
+    const uint64_t rlen = (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
+    cudaStream_t st = ctx->stream;
+    if (plan->host_blocks && !plan->resident) {
+      if (row_ptr) std::memcpy(row_ptr, plan->h_rowptr + B.ro, rlen * 4);
+      if (col) std::memcpy(col, plan->h_cols + B.e0, B.nnz * 4);
+      if (row) std::memcpy(row, plan->h_rows + B.e0, B.nnz * 4);
+      return;
+    }
+    if (row_ptr) BBTC_CUDA(cudaMemcpyAsync(row_ptr, plan->rowptr.p + B.ro, rlen * 4, cudaMemcpyDeviceToHost, st));
+    if (col && B.nnz) BBTC_CUDA(cudaMemcpyAsync(col, plan->cols.p + B.e0, B.nnz * 4, cudaMemcpyDeviceToHost, st));
+    if (row && B.nnz) BBTC_CUDA(cudaMemcpyAsync(row, plan->rows.p + B.e0, B.nnz * 4, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
+  return guard([&] {
+    if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
+    if (plan->host_blocks) return;
+    const uint64_t ro = rowptr_len(plan);
+    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_cols, std::max<uint64_t>(plan->m, 1) * 4, cudaHostAllocPortable));
+    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rows, std::max<uint64_t>(plan->m, 1) * 4, cudaHostAllocPortable));
+    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rowptr, std::max<uint64_t>(ro, 1) * 4, cudaHostAllocPortable));
+    cudaStream_t st = ctx->stream;
+    if (plan->m) {
+      BBTC_CUDA(cudaMemcpyAsync(plan->h_cols, plan->cols.p, plan->m * 4, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaMemcpyAsync(plan->h_rows, plan->rows.p, plan->m * 4, cudaMemcpyDeviceToHost, st));
+    }
+    BBTC_CUDA(cudaMemcpyAsync(plan->h_rowptr, plan->rowptr.p, ro * 4, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    plan->cols.reset();
+    plan->rows.reset();
+    plan->rowptr.reset();
+    plan->host_blocks = true;
+    plan->resident = false;
+    plan->info.host_blocks = 1;
+  });
+}
+
+BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan) {
+  return guard([&] {
+    if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
+    if (plan->resident) return;
+    ensure_device_arenas(ctx, plan);
+    Streamer s(ctx, plan);
+    for (uint32_t b = 0; b < plan->blocks.size(); ++b) s.issue(b);
+    for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamSynchronize(cs));
+    plan->resident = true;
+  });
+}
+
+BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
+  return guard([&] {
+    if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
+    if (!plan->host_blocks) return;   // device plans own their only copy
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+    plan->cols.reset();
+    plan->rows.reset();
+    plan->rowptr.reset();
+    plan->resident = false;
+  });
+}
+
+BBTC_API void bbtc_plan_free(bbtc_plan* plan) {
+  if (!plan) return;
+  if (plan->ctx) cudaStreamSynchronize(plan->ctx->stream);
+  if (plan->h_cols) cudaFreeHost(plan->h_cols);
+  if (plan->h_rows) cudaFreeHost(plan->h_rows);
+  if (plan->h_rowptr) cudaFreeHost(plan->h_rowptr);
+  delete plan;
+}
+
+BBTC_API uint64_t bbtc_n_tasks(uint32_t p) { return n_tasks(p); }
+
+BBTC_API bbtc_status bbtc_task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k, uint64_t* idx) {
+  return guard([&] {
+    if (!idx) raise(BBTC_EINVAL, "idx is NULL");
+    if (!(i <= j && j <= k && k < p)) raise(BBTC_EINVAL, "need i <= j <= k < p");
+    *idx = task_index(p, i, j, k);
+  });
+}
+
+BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32_t* j, uint32_t* k) {
+  return guard([&] {
+    if (!i || !j || !k) raise(BBTC_EINVAL, "NULL argument");
+    if (idx >= n_tasks(p)) raise(BBTC_EINVAL, "idx >= n_tasks(p)");
+    // Invert the closed form: find i, then j, then k by monotone search.
+    uint32_t a = 0;
+    while (a + 1 < p && task_index(p, a + 1, a + 1, a + 1) <= idx) ++a;
+    uint32_t b = a;
+    while (b + 1 < p && task_index(p, a, b + 1, b + 1) <= idx) ++b;
+    *i = a;
+    *j = b;
+    *k = b + (uint32_t)(idx - task_index(p, a, b, b));
+  });
+}
+
+BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
+                                      uint64_t* d_counts) {
+  return guard([&] {
+    if (!ctx || !plan || !d_counts) raise(BBTC_EINVAL, "NULL argument");
+    if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
+    if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident: call bbtc_stage or bbtc_count");
+    count_zero(ctx, plan, d_counts);
+    count_launch(ctx, plan, rank, world, d_counts, 0, plan->item_start.back());
+  });
+}
+
+BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t rank, uint32_t world, uint32_t flags,
+                                uint64_t* total, uint64_t* per_task, bbtc_timing* tm) {
+  return guard([&] {
+    (void)flags;
+    if (!ctx || !cplan || !total) raise(BBTC_EINVAL, "NULL argument");
+    if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
+    bbtc_plan* plan = const_cast<bbtc_plan*>(cplan);   // residency state only
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    const auto t0 = std::chrono::steady_clock::now();
+    const uint64_t l0 = ctx->launches;
+    const uint64_t nt = plan->info.n_tasks;
+    DevBuf<uint64_t> d_counts;
+    d_counts.alloc(nt + 1, ctx->stream);
+    cudaEvent_t k0, k1;
+    BBTC_CUDA(cudaEventCreate(&k0));
+    BBTC_CUDA(cudaEventCreate(&k1));
+    count_zero(ctx, plan, d_counts.p);
+    uint64_t h2d = 0;
+    BBTC_CUDA(cudaEventRecord(k0, ctx->stream));
+    if (plan->resident) {
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back());
+    } else {
+      // a6: stream blocks in execution order, launching each run of ready tasks.
+      ensure_device_arenas(ctx, plan);
+      Streamer s(ctx, plan);
+      const size_t ne = plan->tasks.size();
+      size_t run0 = 0;
+      auto flush = [&](size_t run1) {
+        if (run1 <= run0) return;
+        for (size_t t = run0; t < run1; ++t)
+          for (uint32_t b : {plan->tasks[t].ij, plan->tasks[t].ik, plan->tasks[t].jk})
+            BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, s.ev[b], 0));
+        count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[run0], plan->item_start[run1]);
+        run0 = run1;
+      };
+      for (size_t t = 0; t < ne; ++t) {
+        const TaskDesc& T = plan->tasks[t];
+        bool fresh = !s.issued[T.ij] || !s.issued[T.ik] || !s.issued[T.jk];
+        if (fresh) flush(t);   // tasks before t only need blocks already issued
+        s.issue(T.ij);
+        s.issue(T.ik);
+        s.issue(T.jk);
+      }
+      flush(ne);
+      h2d = s.bytes;
+      plan->resident = true;
+    }
+    BBTC_CUDA(cudaEventRecord(k1, ctx->stream));
+    std::vector<uint64_t> h(nt + 1);
+    BBTC_CUDA(cudaMemcpyAsync(h.data(), d_counts.p, (nt + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+    *total = h[nt];
+    if (per_task) std::copy(h.begin(), h.begin() + nt, per_task);
+    float kms = 0;
+    BBTC_CUDA(cudaEventElapsedTime(&kms, k0, k1));
+    cudaEventDestroy(k0);
+    cudaEventDestroy(k1);
+    if (tm) {
+      tm->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      tm->t_kernel_ms = kms;
+      tm->t_h2d_ms = 0;
+      tm->h2d_bytes = h2d;
+      tm->launches = ctx->launches - l0;
+    }
+  });
+}
+
+}  // extern "C"

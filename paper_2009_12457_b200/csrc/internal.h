@@ -1,0 +1,153 @@
+// internal.h — shared internals of libbbtc (host runtime + kernels).  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bbtc.h"
+
+namespace bbtc {
+
+// ---- error plumbing -----------------------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+  bbtc_status code;
+  std::string msg;
+};
+[[noreturn]] void raise(bbtc_status code, const std::string& msg);
+#define BBTC_CUDA(call)                                                                        \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      ::bbtc::raise(e_ == cudaErrorMemoryAllocation ? BBTC_ENOMEM : BBTC_ECUDA,                \
+                    std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+#define BBTC_LAUNCHED(ctx)                                                                     \
+  do {                                                                                         \
+    BBTC_CUDA(cudaGetLastError());                                                             \
+    (ctx)->launches++;                                                                         \
+  } while (0)
+
+// ---- device buffers (stream-ordered pool allocations) -------------------------------
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void alloc(size_t count, cudaStream_t stream) {
+    reset();
+    s = stream;
+    n = count;
+    if (count) BBTC_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+  }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+struct bbtc_ctx_impl;
+
+}  // namespace bbtc
+
+struct bbtc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<cudaStream_t> copy_streams;
+  uint64_t launches = 0;
+  int sm_count = 148;
+  void* cursor = nullptr;          // device scratch: work-item cursors of the count kernel
+  uint64_t cursor_next = 0;
+};
+constexpr int kCursorSlots = 1024;
+
+struct bbtc_graph {
+  bbtc_ctx* ctx = nullptr;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  uint64_t raw = 0;
+  uint32_t d_max = 0;
+  uint32_t n_nonisolated = 0;
+  bbtc::DevBuf<uint32_t> deg_sorted;  // full degrees in rank order (n)
+  bbtc::DevBuf<uint32_t> rank;        // rank of each input id (n)
+  bbtc::DevBuf<uint64_t> okeys;       // oriented edges (ru << 32 | rw), ru < rw, unsorted (m)
+};
+
+// One upper-triangular block G_ij in the arena (column-major block order:
+// b = j(j+1)/2 + i).
+struct BlockDesc {
+  uint64_t e0;      // first edge (index into cols / rows arenas)
+  uint64_t nnz;     // edges
+  uint64_t ro;      // first row offset (index into rowptr arena); |V_i|+1 entries
+  uint32_t i, j;
+};
+
+// Task (i,j,k) as the count kernel sees it.
+struct TaskDesc {
+  uint32_t ij, ik, jk;  // block ids
+  uint32_t idx;         // canonical Alg. 4 index
+};
+
+struct bbtc_plan {
+  uint32_t p = 0;
+  uint32_t clamped = 0;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  std::vector<uint32_t> cuts;
+  std::vector<BlockDesc> blocks;
+  std::vector<TaskDesc> tasks;        // in execution order
+  std::vector<uint64_t> item_start;   // prefix over tasks (execution order) of work items
+  uint32_t chunk = 0;                 // edges per work item
+  bbtc_plan_info info{};
+  // device arenas
+  bbtc::DevBuf<uint32_t> cols;        // m: local column id v - cuts[j]
+  bbtc::DevBuf<uint32_t> rows;        // m: local row id u - cuts[i]
+  bbtc::DevBuf<uint32_t> rowptr;      // sum over blocks of |V_i|+1
+  bbtc::DevBuf<BlockDesc> d_blocks;
+  bbtc::DevBuf<TaskDesc> d_tasks;
+  bbtc::DevBuf<uint64_t> d_item_start;
+  // pinned host copies (bbtc_plan_to_host)
+  bool host_blocks = false;
+  uint32_t* h_cols = nullptr;
+  uint32_t* h_rows = nullptr;
+  uint32_t* h_rowptr = nullptr;
+  bool resident = true;               // device arenas hold every block
+  bbtc_ctx* ctx = nullptr;
+};
+
+namespace bbtc {
+// prep.cu
+void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint,
+                 int mem, bbtc_graph* g);
+void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col);
+void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,
+                bbtc_plan* plan);
+// count.cu
+void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
+void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
+                  uint64_t item_lo, uint64_t item_hi);
+void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
+// capi.cpp (host)
+uint64_t n_tasks(uint32_t p);
+uint64_t task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k);
+inline uint32_t block_id(uint32_t i, uint32_t j) { return j * (j + 1) / 2 + i; }
+void plan_tasks(bbtc_plan* plan, uint32_t world);
+}  // namespace bbtc

@@ -1,0 +1,497 @@
+// prep.cu — device preprocessing: steps a1-a5 of the hot path.
+//
+//   a1 canonicalise   raw pairs -> sorted unique (min,max) keys
+//   a2 degree order   full degrees, stable rank by (degree, id), orient
+//   a3 partition      symmetric cut vector (full-degree prefix rule)
+//   a4 BCSR           p(p+1)/2 upper blocks, local ids, row offsets        P:460-463, Fig. 2d
+//   a5 tasks          Alg. 4 enumeration + work items (host, capi.cpp)
+//
+// Everything is HBM-bandwidth work: streaming passes, one radix sort per phase
+// (CUB onesweep, the library primitive for sorting) and scatter/gather kernels
+// sized as grid-stride loops over the SM count.
+#include <cub/cub.cuh>
+#include <thrust/iterator/reverse_iterator.h>
+
+#include <algorithm>
+#include <chrono>
+
+#include "internal.h"
+
+namespace bbtc {
+namespace {
+
+constexpr uint64_t kSentinel = ~0ull;
+constexpr int kThreads = 256;
+
+inline int bitlen(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+inline unsigned grid_for(const bbtc_ctx* ctx, uint64_t n, int per_sm = 8) {
+  uint64_t want = (n + kThreads - 1) / kThreads;
+  uint64_t cap = (uint64_t)ctx->sm_count * per_sm;
+  return (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+template <class F>
+void cub_call(bbtc_ctx* ctx, F f) {
+  size_t bytes = 0;
+  BBTC_CUDA(f((void*)nullptr, bytes));
+  DevBuf<uint8_t> tmp;
+  tmp.alloc(std::max<size_t>(bytes, 1), ctx->stream);
+  BBTC_CUDA(f((void*)tmp.p, bytes));
+  ctx->launches += 1;
+}
+
+// ---- a1 ------------------------------------------------------------------------------
+// key = (min << 32) | max for a != b, kSentinel for self-loops; tracks the largest id.
+__global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t E,
+                        uint64_t* __restrict__ keys, uint32_t* __restrict__ max_id) {
+  uint32_t mx = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t a = src[e], b = dst[e];
+    uint32_t lo = min(a, b), hi = max(a, b);
+    mx = max(mx, hi);
+    keys[e] = a == b ? kSentinel : ((uint64_t)lo << 32) | hi;
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
+}
+
+// ---- a2 ------------------------------------------------------------------------------
+__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ deg) {
+  // Warp-uniform trip count so the whole warp stays converged for __match_any_sync.
+  const uint64_t lane = threadIdx.x & 31;
+  const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = warp0; base < m; base += stride) {
+    const uint64_t e = base + lane;
+    const bool valid = e < m;
+    const uint64_t k = valid ? keys[e] : 0;
+    const uint32_t lo = valid ? (uint32_t)(k >> 32) : 0xFFFFFFFFu, hi = (uint32_t)k;
+    // Keys are sorted, so equal `lo` values sit in the same warp: aggregate them.
+    const uint32_t peers = __match_any_sync(0xffffffffu, lo);
+    if (valid && lane == (uint64_t)(__ffs(peers) - 1)) atomicAdd(&deg[lo], __popc(peers));
+    if (valid) atomicAdd(&deg[hi], 1u);
+  }
+}
+
+__global__ void k_iota(uint32_t* __restrict__ x, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = i;
+}
+
+__global__ void k_rank(const uint32_t* __restrict__ order, uint32_t n, uint32_t* __restrict__ rank) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) rank[order[r]] = r;
+}
+
+// Orientation from lower to higher degree rank (P:226-235 with the order of P:438-446).
+__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, const uint32_t* __restrict__ rank,
+                         uint64_t* __restrict__ okeys) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[e];
+    uint32_t ra = rank[(uint32_t)(k >> 32)], rb = rank[(uint32_t)k];
+    okeys[e] = ((uint64_t)min(ra, rb) << 32) | max(ra, rb);
+  }
+}
+
+__global__ void k_graph_stats(const uint32_t* __restrict__ deg_sorted, uint32_t n, uint32_t* out) {
+  // out[0] = first rank with degree > 0 (binary search), out[1] = d_max.
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      uint32_t mid = lo + (hi - lo) / 2;
+      if (deg_sorted[mid] == 0) lo = mid + 1; else hi = mid;
+    }
+    out[0] = lo;
+    out[1] = n ? deg_sorted[n - 1] : 0;
+  }
+}
+
+// ---- a3 ------------------------------------------------------------------------------
+struct ToU64 {
+  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
+// cuts[i] = max(cuts[i-1], min{ r : P[r] >= ceil(i*2m/p) }), P[r] = sum of the first r
+// rank-ordered degrees (P[0] = 0, P[n] = 2m).  incl[r] = P[r+1].
+__global__ void k_cuts(const uint64_t* __restrict__ incl, uint32_t n, uint64_t two_m, uint32_t p,
+                       uint32_t* __restrict__ cuts) {
+  for (uint32_t i = 1 + threadIdx.x; i < p; i += blockDim.x) {
+    uint64_t target = ((uint64_t)i * two_m + p - 1) / p;
+    // smallest r in [0, n] with P[r] >= target
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      uint32_t mid = lo + (hi - lo) / 2;
+      uint64_t P = mid == 0 ? 0 : incl[mid - 1];
+      if (P >= target) hi = mid; else lo = mid + 1;
+    }
+    cuts[i] = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cuts[0] = 0;
+    for (uint32_t i = 1; i < p; ++i) cuts[i] = max(cuts[i], cuts[i - 1]);
+    cuts[p] = n;
+  }
+}
+
+// ---- a4 ------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t part_of(const uint32_t* cuts, uint32_t p, uint32_t r) {
+  // the i with cuts[i] <= r < cuts[i+1] (largest i with cuts[i] <= r)
+  uint32_t lo = 0, hi = p - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi + 1) / 2;
+    if (cuts[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Block sort key: (j, ru, rw) with j = part(rw).  Sorting by it lays the blocks out
+// contiguously in column-major block order, rows ascending inside a block and the
+// columns of each row ascending (what Alg. 1 needs: "A and B are sorted").
+__global__ void k_block_keys(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
+                             uint32_t p, int bn, uint64_t* __restrict__ ckeys) {
+  extern __shared__ uint32_t s_cuts[];
+  for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = okeys[e];
+    uint64_t ru = k >> 32, rw = (uint32_t)k;
+    uint64_t j = part_of(s_cuts, p, (uint32_t)rw);
+    ckeys[e] = (j << (2 * bn)) | (ru << bn) | rw;
+  }
+}
+
+// Block b = (i,j) starts at the first key >= (j, cuts[i], 0).
+__global__ void k_block_starts(const uint64_t* __restrict__ ckeys, uint64_t m, const uint32_t* __restrict__ cuts,
+                               uint32_t p, int bn, uint64_t* __restrict__ starts) {
+  uint32_t nb = p * (p + 1) / 2;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += gridDim.x * blockDim.x) {
+    if (b == nb) { starts[b] = m; continue; }
+    uint32_t j = 0;
+    while ((j + 1) * (j + 2) / 2 <= b) ++j;
+    uint32_t i = b - j * (j + 1) / 2;
+    uint64_t probe = ((uint64_t)j << (2 * bn)) | ((uint64_t)cuts[i] << bn);
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      uint64_t mid = lo + (hi - lo) / 2;
+      if (ckeys[mid] < probe) lo = mid + 1; else hi = mid;
+    }
+    starts[b] = lo;
+  }
+}
+
+// Local ids: cols[e] = rw - cuts[j], rows[e] = ru - cuts[i]; and the row-start marks.
+__global__ void k_split(const uint64_t* __restrict__ ckeys, uint64_t m, const uint32_t* __restrict__ gcuts,
+                        uint32_t p, int bn, const BlockDesc* __restrict__ blocks, uint32_t* __restrict__ cols,
+                        uint32_t* __restrict__ rows, uint32_t* __restrict__ rowptr) {
+  extern __shared__ uint32_t s_cuts[];
+  for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+  __syncthreads();
+  const uint64_t mask = (1ull << bn) - 1;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = ckeys[e];
+    uint32_t j = (uint32_t)(k >> (2 * bn));
+    uint32_t ru = (uint32_t)((k >> bn) & mask), rw = (uint32_t)(k & mask);
+    uint32_t i = part_of(s_cuts, p, ru);
+    uint32_t lr = ru - s_cuts[i];
+    cols[e] = rw - s_cuts[j];
+    rows[e] = lr;
+    const BlockDesc& B = blocks[j * (j + 1) / 2 + i];
+    bool first = e == B.e0;
+    if (!first) {
+      uint64_t kp = ckeys[e - 1];
+      first = ((kp >> bn) & mask) != ru;
+    }
+    if (first) rowptr[B.ro + lr] = (uint32_t)e;   // global edge index of the row's first edge
+  }
+}
+
+// Row-offset arena entry |V_i| of every block = the block's end (global index).
+__global__ void k_row_ends(const BlockDesc* __restrict__ blocks, uint32_t nb, const uint32_t* __restrict__ cuts,
+                           uint32_t* __restrict__ rowptr) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const BlockDesc& B = blocks[b];
+    rowptr[B.ro + (cuts[B.i + 1] - cuts[B.i])] = (uint32_t)(B.e0 + B.nnz);
+  }
+}
+
+struct MinOp {
+  __host__ __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a < b ? a : b; }
+};
+
+// Global -> block-local offsets.  grid.y walks the blocks.
+__global__ void k_row_local(const BlockDesc* __restrict__ blocks, const uint32_t* __restrict__ cuts,
+                            uint32_t* __restrict__ rowptr) {
+  const BlockDesc B = blocks[blockIdx.y];
+  const uint32_t len = cuts[B.i + 1] - cuts[B.i] + 1;
+  const uint32_t base = (uint32_t)B.e0;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < len; r += gridDim.x * blockDim.x)
+    rowptr[B.ro + r] -= base;
+}
+
+}  // namespace
+
+// =====================================================================================
+void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint, int mem,
+                 bbtc_graph* g) {
+  cudaStream_t st = ctx->stream;
+  g->raw = E;
+  DevBuf<uint32_t> dmax;
+  dmax.alloc(2, st);
+  BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
+  DevBuf<uint64_t> keys;
+  keys.alloc(E, st);
+  if (E) {
+    if (mem == BBTC_MEM_DEVICE) {
+      k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, keys.p, dmax.p);
+      BBTC_LAUNCHED(ctx);
+    } else {
+      // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
+      const uint64_t chunk = 1ull << 25;   // 32 Mi pairs = 256 MiB per chunk
+      DevBuf<uint32_t> ds, dd;
+      ds.alloc(std::min(E, 2 * chunk), st);
+      dd.alloc(std::min(E, 2 * chunk), st);
+      cudaStream_t cs = ctx->copy_streams[0];
+      cudaEvent_t ev_copied[2], ev_used[2];
+      for (int x = 0; x < 2; ++x) {
+        BBTC_CUDA(cudaEventCreateWithFlags(&ev_copied[x], cudaEventDisableTiming));
+        BBTC_CUDA(cudaEventCreateWithFlags(&ev_used[x], cudaEventDisableTiming));
+        BBTC_CUDA(cudaEventRecord(ev_used[x], st));
+      }
+      for (uint64_t c0 = 0, it = 0; c0 < E; c0 += chunk, ++it) {
+        const uint64_t len = std::min(chunk, E - c0);
+        const int slot = it & 1;
+        BBTC_CUDA(cudaStreamWaitEvent(cs, ev_used[slot], 0));
+        BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
+        BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
+        BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
+        BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
+        k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(ds.p + slot * chunk, dd.p + slot * chunk, len, keys.p + c0,
+                                                          dmax.p);
+        BBTC_LAUNCHED(ctx);
+        BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
+      }
+      for (int x = 0; x < 2; ++x) {
+        cudaEventDestroy(ev_copied[x]);
+        cudaEventDestroy(ev_used[x]);
+      }
+    }
+  }
+  uint32_t max_id = 0;
+  BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  if (E && max_id == 0xFFFFFFFFu) raise(BBTC_ERANGE, "vertex id 0xFFFFFFFF is reserved");
+  const uint32_t n = E ? std::max<uint32_t>(n_hint, max_id + 1) : n_hint;
+  g->n = n;
+  const int bid = std::max(1, bitlen(max_id));
+  // Sort the canonical keys over their live bits (hi id in [0,bid), lo id in [32,32+bid)).
+  uint64_t m = 0;
+  DevBuf<uint64_t> ukeys;
+  if (E) {
+    DevBuf<uint64_t> alt;
+    alt.alloc(E, st);
+    cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, 32 + bid, st);
+    });
+    DevBuf<uint64_t>& sorted = db.Current() == keys.p ? keys : alt;
+    DevBuf<uint64_t>& other = db.Current() == keys.p ? alt : keys;
+    DevBuf<uint64_t> nsel;
+    nsel.alloc(1, st);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Unique(t, b, sorted.p, other.p, nsel.p, E, st);
+    });
+    uint64_t cnt = 0, last = 0;
+    BBTC_CUDA(cudaMemcpyAsync(&cnt, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    if (cnt) {
+      BBTC_CUDA(cudaMemcpyAsync(&last, other.p + cnt - 1, 8, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaStreamSynchronize(st));
+    }
+    m = cnt - (cnt && last == kSentinel ? 1 : 0);
+    ukeys = std::move(other);
+    sorted.reset();
+  }
+  if (m >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
+  g->m = m;
+  // Degrees and stable degree rank.
+  DevBuf<uint32_t> deg;
+  deg.alloc(n, st);
+  g->deg_sorted.alloc(n, st);
+  g->rank.alloc(n, st);
+  g->okeys.alloc(m, st);
+  if (n) {
+    BBTC_CUDA(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
+    if (m) {
+      k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, deg.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    DevBuf<uint32_t> ids, order;
+    ids.alloc(n, st);
+    order.alloc(n, st);
+    k_iota<<<grid_for(ctx, n), kThreads, 0, st>>>(ids.p, n);
+    BBTC_LAUNCHED(ctx);
+    const int bdeg = std::max(1, bitlen(std::min<uint64_t>(m, n - 1)));
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, deg.p, g->deg_sorted.p, ids.p, order.p, (uint64_t)n, 0, bdeg, st);
+    });
+    k_rank<<<grid_for(ctx, n), kThreads, 0, st>>>(order.p, n, g->rank.p);
+    BBTC_LAUNCHED(ctx);
+    if (m) {
+      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, g->rank.p, g->okeys.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    k_graph_stats<<<1, 32, 0, st>>>(g->deg_sorted.p, n, dmax.p);
+    BBTC_LAUNCHED(ctx);
+    uint32_t h[2];
+    BBTC_CUDA(cudaMemcpyAsync(h, dmax.p, 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    g->n_nonisolated = n - h[0];
+    g->d_max = h[1];
+  }
+}
+
+void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col) {
+  cudaStream_t st = ctx->stream;
+  std::vector<uint64_t> keys(g->m);
+  if (g->m) {
+    DevBuf<uint64_t> a, b;
+    a.alloc(g->m, st);
+    b.alloc(g->m, st);
+    BBTC_CUDA(cudaMemcpyAsync(a.p, g->okeys.p, g->m * 8, cudaMemcpyDeviceToDevice, st));
+    cub::DoubleBuffer<uint64_t> db(a.p, b.p);
+    cub_call(ctx, [&](void* t, size_t& bb) { return cub::DeviceRadixSort::SortKeys(t, bb, db, g->m, 0, 64, st); });
+    BBTC_CUDA(cudaMemcpyAsync(keys.data(), db.Current(), g->m * 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  }
+  std::fill(row_ptr, row_ptr + (uint64_t)g->n + 1, 0);
+  for (uint64_t e = 0; e < g->m; ++e) {
+    row_ptr[(keys[e] >> 32) + 1]++;
+    col[e] = (uint32_t)keys[e];
+  }
+  for (uint32_t u = 0; u < g->n; ++u) row_ptr[u + 1] += row_ptr[u];
+}
+
+void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,
+                bbtc_plan* plan) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  plan->n = n;
+  plan->m = m;
+  plan->ctx = ctx;
+  // ---- a3: cuts
+  uint32_t pe;
+  if (user_cuts) {
+    pe = p;
+    if (user_cuts[0] != 0 || user_cuts[p] != n) raise(BBTC_EINVAL, "cuts must satisfy cuts[0] = 0 and cuts[p] = n");
+    for (uint32_t i = 0; i < p; ++i)
+      if (user_cuts[i] > user_cuts[i + 1]) raise(BBTC_EINVAL, "cuts must be non-decreasing");
+    plan->cuts.assign(user_cuts, user_cuts + p + 1);
+  } else {
+    pe = n == 0 ? 1 : std::min(p, n);
+    plan->clamped = pe != p;
+    plan->cuts.assign(pe + 1, 0);
+    plan->cuts[pe] = n;
+    if (n > 0 && pe > 1) {
+      DevBuf<uint64_t> incl;
+      incl.alloc(n, st);
+      cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(g->deg_sorted.p, ToU64{});
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceScan::InclusiveSum(t, b, it, incl.p, (uint64_t)n, st);
+      });
+      DevBuf<uint32_t> dc;
+      dc.alloc(pe + 1, st);
+      k_cuts<<<1, 256, 0, st>>>(incl.p, n, 2 * m, pe, dc.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaMemcpyAsync(plan->cuts.data(), dc.p, (pe + 1) * 4, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  plan->p = pe;
+  const uint32_t nb = pe * (pe + 1) / 2;
+  const int bn = std::max(1, bitlen(n ? n - 1 : 0));
+  const int bp = bitlen(pe - 1);
+  if (bp + 2 * bn > 64) raise(BBTC_ERANGE, "n and p too large for the 64-bit block sort key");
+  DevBuf<uint32_t> dcuts;
+  dcuts.alloc(pe + 1, st);
+  BBTC_CUDA(cudaMemcpyAsync(dcuts.p, plan->cuts.data(), (pe + 1) * 4, cudaMemcpyHostToDevice, st));
+  // ---- a4: block-ordered keys
+  DevBuf<uint64_t> ck, ck_alt;
+  ck.alloc(m, st);
+  std::vector<uint64_t> starts(nb + 1, 0);
+  const size_t cut_smem = (pe + 1) * 4;
+  if (m) {
+    k_block_keys<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(g->okeys.p, m, dcuts.p, pe, bn, ck.p);
+    BBTC_LAUNCHED(ctx);
+    ck_alt.alloc(m, st);
+    cub::DoubleBuffer<uint64_t> db(ck.p, ck_alt.p);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, db, m, 0, bp + 2 * bn, st);
+    });
+    if (db.Current() != ck.p) std::swap(ck, ck_alt);
+    ck_alt.reset();
+    DevBuf<uint64_t> dstarts;
+    dstarts.alloc(nb + 1, st);
+    k_block_starts<<<(nb + 1 + 127) / 128, 128, 0, st>>>(ck.p, m, dcuts.p, pe, bn, dstarts.p);
+    BBTC_LAUNCHED(ctx);
+    BBTC_CUDA(cudaMemcpyAsync(starts.data(), dstarts.p, (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  }
+  // Block table (column-major: b = j(j+1)/2 + i).
+  plan->blocks.resize(nb);
+  uint64_t ro = 0, m_max = 0, bytes = 0;
+  for (uint32_t j = 0; j < pe; ++j)
+    for (uint32_t i = 0; i <= j; ++i) {
+      uint32_t b = block_id(i, j);
+      BlockDesc& B = plan->blocks[b];
+      B.i = i;
+      B.j = j;
+      B.e0 = starts[b];
+      B.nnz = starts[b + 1] - starts[b];
+      B.ro = ro;
+      ro += (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
+      m_max = std::max(m_max, B.nnz);
+      bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1);
+    }
+  plan->cols.alloc(m, st);
+  plan->rows.alloc(m, st);
+  plan->rowptr.alloc(ro, st);
+  plan->d_blocks.alloc(nb, st);
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0xFF, ro * 4, st));
+  if (m) {
+    k_split<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(ck.p, m, dcuts.p, pe, bn, plan->d_blocks.p, plan->cols.p,
+                                                          plan->rows.p, plan->rowptr.p);
+    BBTC_LAUNCHED(ctx);
+  }
+  ck.reset();
+  k_row_ends<<<(nb + 127) / 128, 128, 0, st>>>(plan->d_blocks.p, nb, dcuts.p, plan->rowptr.p);
+  BBTC_LAUNCHED(ctx);
+  // Empty rows take the start of the next non-empty row: reverse inclusive min-scan.
+  {
+    thrust::reverse_iterator<uint32_t*> rin(plan->rowptr.p + ro);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::InclusiveScan(t, b, rin, rin, MinOp{}, (uint64_t)ro, st);
+    });
+  }
+  {
+    uint32_t maxv = 0;
+    for (uint32_t i = 0; i < pe; ++i) maxv = std::max(maxv, plan->cuts[i + 1] - plan->cuts[i] + 1);
+    dim3 grid(std::max(1u, std::min((maxv + kThreads - 1) / kThreads, 64u)), nb);
+    k_row_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dcuts.p, plan->rowptr.p);
+    BBTC_LAUNCHED(ctx);
+  }
+  // ---- a5: tasks and work items (host)
+  plan->info.p = pe;
+  plan->info.clamped = plan->clamped;
+  plan->info.n_tasks = n_tasks(pe);
+  plan->info.n_blocks = nb;
+  plan->info.m = m;
+  plan->info.m_max = m_max;
+  plan->info.lambda = m ? (double)m_max / (2.0 * (double)m / ((double)pe * (pe + 1))) : 0.0;
+  plan->info.block_bytes = bytes;
+  plan_tasks(plan, 1);
+  if (flags & BBTC_PLAN_STATS) plan_stats(ctx, plan);
+}
+
+}  // namespace bbtc

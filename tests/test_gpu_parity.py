@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, bit-exact.
+
+Every count is an integer, so totals and per-task counts must match exactly
+(SURVEY.md §8(c) A18).  Inputs are seeded and synthetic (inputs/).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ctx(gpu):
+    import paper_2009_12457_b200 as bb
+    return bb.Context(0)
+
+
+def run(ctx, s, d, n_hint, p=1, cuts=None, stats=False):
+    import paper_2009_12457_b200 as bb
+    g = bb.Graph.from_edges(ctx, s, d, n_hint)
+    plan = bb.Plan(ctx, g, p, cuts, stats=stats)
+    tot, pt = plan.count()
+    return g, plan, tot, pt
+
+
+def check(ctx, s, d, n_hint, p=1, cuts=None, og=None):
+    og = og or oracle.OracleGraph(s, d, n_hint)
+    g, plan, tot, pt = run(ctx, s, d, n_hint, p, cuts)
+    ocuts = og.default_cuts(p) if cuts is None else np.asarray(cuts, np.uint32)
+    assert np.array_equal(plan.cuts(), ocuts)
+    otot, opt, _, _ = og.count(cuts=ocuts)
+    assert tot == otot
+    assert np.array_equal(pt, opt)
+    return g, plan
+
+
+def test_karate_golden(ctx):
+    G = json.load(open(os.path.join(GOLD, "karate.json")))
+    s, d = inputs.karate()
+    g, plan, tot, pt = run(ctx, s, d, 34, 2)
+    assert tot == G["total"] == 45
+    assert list(plan.cuts()) == G["default_cuts"]["2"]
+    rank = g.rank()
+    order = np.empty(34, np.int64)
+    order[rank] = np.arange(34)
+    assert list(order) == G["order_new_to_old"]
+    for case in G["per_task"]:
+        _, _, tot, pt = run(ctx, s, d, 34, cuts=case["cuts"])
+        assert list(pt) == case["counts"] and tot == 45
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_rmat16_p_grid(ctx, seed):
+    s, d = inputs.rmat(16, 16, seed)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    for p in (1, 2, 3, 4, 5, 8, 16):
+        check(ctx, s, d, 1 << 16, p, og=og)
+
+
+def test_rmat16_preprocessing_matches_oracle(ctx):
+    s, d = inputs.rmat(16, 16, 1)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    import paper_2009_12457_b200 as bb
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 16)
+    st = g.stats()
+    assert (st["n"], st["m"]) == (og.n, og.m)
+    assert st["d_max"] == int(og.degrees().max())
+    assert st["n_nonisolated"] == int((og.degrees() > 0).sum())
+    assert np.array_equal(g.rank(), og.rank())
+    row, col = g.csr()
+    orow, ocol = og.csr()
+    assert np.array_equal(row, orow) and np.array_equal(col, ocol)
+
+
+def test_blocks_round_trip(ctx):
+    """Every block G_ij holds exactly the oriented edges with u in V_i, v in V_j."""
+    s, d = inputs.rmat(12, 16, 4)
+    og = oracle.OracleGraph(s, d, 1 << 12)
+    g, plan, _, _ = run(ctx, s, d, 1 << 12, 5)
+    cuts = plan.cuts()
+    orow, ocol = og.csr()
+    src = np.repeat(np.arange(og.n), np.diff(orow).astype(np.int64))
+    seen = 0
+    for j in range(5):
+        for i in range(j + 1):
+            rp, col, row = plan.block(i, j)
+            assert rp[0] == 0 and rp[-1] == len(col) and np.all(np.diff(rp.astype(np.int64)) >= 0)
+            assert np.array_equal(np.repeat(np.arange(len(rp) - 1), np.diff(rp).astype(np.int64)), row)
+            sel = (src >= cuts[i]) & (src < cuts[i + 1]) & (ocol >= cuts[j]) & (ocol < cuts[j + 1])
+            assert np.array_equal(row.astype(np.int64) + cuts[i], src[sel])
+            assert np.array_equal(col.astype(np.int64) + cuts[j], ocol[sel].astype(np.int64))
+            seen += len(col)
+    assert seen == og.m
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_graphs_random_cuts(ctx, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 400))
+    s, d = inputs.gnp(n, float(rng.uniform(0.02, 0.4)), seed=seed)
+    og = oracle.OracleGraph(s, d, n)
+    for p in (1, 2, 3, 6):
+        inner = np.sort(rng.integers(0, og.n + 1, size=p - 1))
+        cuts = np.concatenate([[0], inner, [og.n]]).astype(np.uint32)
+        check(ctx, s, d, n, cuts=cuts, og=og)
+        check(ctx, s, d, n, p=p, og=og)
+
+
+def test_dense_rows_exceed_slab(ctx):
+    """K_n with long rows forces the global-memory search path (|A_u| > 1024 words)."""
+    n = 1400
+    iu = np.triu_indices(n, 1)
+    s, d = iu[0].astype(np.uint32), iu[1].astype(np.uint32)
+    g, plan, tot, pt = run(ctx, s, d, n, 1)
+    assert tot == n * (n - 1) * (n - 2) // 6
+    _, _, tot3, pt3 = run(ctx, s, d, n, cuts=[0, 300, 1400])
+    sz = [300, 1100]
+    want = [300 * 299 * 298 // 6, 300 * 299 // 2 * 1100, 300 * 1100 * 1099 // 2, 1100 * 1099 * 1098 // 6]
+    assert list(pt3) == want and tot3 == tot
+
+
+def test_degenerate_inputs(ctx):
+    import paper_2009_12457_b200 as bb
+    e = np.zeros(0, np.uint32)
+    _, plan, tot, pt = run(ctx, e, e, 0, 3)
+    assert tot == 0 and plan.p == 1
+    _, plan, tot, pt = run(ctx, e, e, 9, 4)
+    assert tot == 0 and plan.p == 4 and len(pt) == 20
+    loops = np.array([1, 5, 5, 7], np.uint32)
+    g, plan, tot, _ = run(ctx, loops, loops, 0, 2)
+    assert tot == 0 and g.stats()["m"] == 0 and g.stats()["n"] == 8
+    tri = np.array([0, 1, 2, 1, 0], np.uint32), np.array([1, 2, 0, 0, 0], np.uint32)
+    g, plan, tot, pt = run(ctx, tri[0], tri[1], 0, 7)          # p > n clamps to n = 3
+    assert tot == 1 and plan.p == 3 and plan.info()["clamped"] == 1 and int(pt.sum()) == 1
+    with pytest.raises(bb.BBTCError):
+        run(ctx, tri[0], tri[1], 0, cuts=[0, 2, 1, 3])           # non-monotone cuts
+    with pytest.raises(bb.BBTCError):
+        run(ctx, tri[0], tri[1], 0, cuts=[0, 2])                 # cuts[p] != n
+    with pytest.raises(bb.BBTCError):
+        run(ctx, tri[0], tri[1], 0, 0)                           # p == 0
+    bad = np.array([0xFFFFFFFF], np.uint32)
+    with pytest.raises(bb.BBTCError):
+        run(ctx, bad, np.array([1], np.uint32), 0, 1)
+
+
+def test_device_input_streaming_and_ranks(ctx):
+    """Device-resident input, host-streamed blocks (a6) and a rank split all agree."""
+    import torch
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(15, 16, 9)
+    og = oracle.OracleGraph(s, d, 1 << 15)
+    otot, opt, _, _ = og.count(cuts=og.default_cuts(6))
+    ts = torch.from_numpy(s.view(np.int32)).cuda()
+    td = torch.from_numpy(d.view(np.int32)).cuda()
+    g = bb.Graph.from_edges(ctx, ts, td, 1 << 15)
+    plan = bb.Plan(ctx, g, 6, stats=True)
+    tot, pt = plan.count()
+    assert tot == otot and np.array_equal(pt, opt)
+    info = plan.info()
+    assert info["b_alg"] > 0 and info["visits"] >= info["m"]
+    # rank split: partial counts sum to the full result
+    acc = np.zeros_like(pt)
+    for r in range(3):
+        t_r, pt_r = plan.count(rank=r, world=3)
+        acc += pt_r
+    assert np.array_equal(acc, opt)
+    # async into a device tensor
+    dc = torch.zeros(plan.n_tasks + 1, dtype=torch.int64, device="cuda")
+    plan.count_async(dc)
+    torch.cuda.synchronize()
+    h = dc.cpu().numpy().view(np.uint64)
+    assert int(h[-1]) == otot and np.array_equal(h[:-1], opt)
+    # out-of-core form: blocks in pinned host memory, streamed on count
+    plan.to_host()
+    assert plan.info()["host_blocks"] == 1
+    tot2, pt2, tm = plan.count(timing=True)
+    assert tot2 == otot and np.array_equal(pt2, opt) and tm["h2d_bytes"] > 0
+    tot3, pt3, tm3 = plan.count(timing=True)           # now resident: no copies
+    assert tot3 == otot and tm3["h2d_bytes"] == 0
+    plan.unstage()
+    plan.stage()
+    assert plan.count()[0] == otot
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["orkut", "rmat24"])
+def test_full_size_configs(ctx, name):
+    """BASELINE.json configs 3 and 4 at full size, whole-result parity with the oracle."""
+    cfg = inputs.CONFIGS[name]
+    s, d = cfg.generate(seed=1)
+    og = oracle.OracleGraph(s, d, cfg.n_hint)
+    check(ctx, s, d, cfg.n_hint, cfg.p, og=og)
