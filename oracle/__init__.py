@@ -50,7 +50,7 @@ def _load():
         L.oracle_count_task.argtypes = [_vp, ctypes.c_uint32, _u32p, ctypes.c_uint32, ctypes.c_uint32,
                                         ctypes.c_uint32, ctypes.c_int, _u64p]
         L.oracle_task_list.argtypes = [ctypes.c_uint32, _u32p, _u32p, _u32p]
-        L.oracle_count_rows.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, _u64p, _u64p]
+        L.oracle_count_rows.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, _u64p, _u64p]
         L.oracle_last_error.restype = ctypes.c_char_p
         _lib = L
     return _lib
@@ -141,11 +141,11 @@ class OracleGraph:
             raise ValueError(_load().oracle_last_error().decode())
         return int(c.value)
 
-    def count_rows(self, u0: int, u1: int):
-        """Unblocked node iterator over rows [u0,u1): (triangles, oriented edges visited)."""
+    def count_rows(self, u0: int, u1: int, stride: int = 1):
+        """Unblocked node iterator over rows u0, u0+stride, ... < u1: (triangles, edges visited)."""
         t = ctypes.c_uint64()
         e = ctypes.c_uint64()
-        _load().oracle_count_rows(self._h, u0, u1, self.threads, ctypes.byref(t), ctypes.byref(e))
+        _load().oracle_count_rows(self._h, u0, u1, stride, self.threads, ctypes.byref(t), ctypes.byref(e))
         return int(t.value), int(e.value)
 
 

@@ -286,15 +286,18 @@ void oracle_task_list(uint32_t p, uint32_t* ti, uint32_t* tj, uint32_t* tk) {
       for (uint32_t k = j; k < p; ++k) { ti[t] = i; tj[t] = j; tk[t] = k; ++t; }
 }
 
-// Timing helper for the CPU baseline: count only rows u in [u0, u1) (unblocked
-// node iterator), returning the triangles found and the merge steps taken.
-int oracle_count_rows(void* h, uint32_t u0, uint32_t u1, int threads, uint64_t* tri, uint64_t* edges) {
+// Timing helper for the CPU baseline: count only rows u = u0, u0+stride, ... < u1
+// (unblocked node iterator), returning the triangles found and the edges visited.
+int oracle_count_rows(void* h, uint32_t u0, uint32_t u1, uint32_t stride, int threads, uint64_t* tri,
+                      uint64_t* edges) {
   Graph* g = (Graph*)h;
   uint64_t tot = 0, ed = 0;
   u1 = std::min(u1, g->n);
+  if (stride == 0) stride = 1;
+  const int64_t cnt = u1 > u0 ? ((int64_t)u1 - u0 + stride - 1) / stride : 0;
 #pragma omp parallel for schedule(dynamic, 256) num_threads(nthreads(threads)) reduction(+ : tot, ed)
-  for (int64_t uu = u0; uu < (int64_t)u1; ++uu) {
-    const uint32_t u = (uint32_t)uu;
+  for (int64_t x = 0; x < cnt; ++x) {
+    const uint32_t u = (uint32_t)(u0 + x * stride);
     const uint32_t* Nu = g->col.data() + g->row[u];
     const uint64_t du = g->row[u + 1] - g->row[u];
     ed += du;

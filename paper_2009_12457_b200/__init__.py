@@ -52,6 +52,11 @@ class Context:
     """A CUDA device + the stream the library enqueues on (bbtc_ctx)."""
 
     def __init__(self, device: int = 0, stream: int | None = None, copy_streams: int = 0):
+        """stream: a cudaStream_t handle (e.g. torch.cuda.Stream().cuda_stream) to enqueue on, or None
+        for a library-created stream.  0 (the legacy default stream) is rejected: the library's own
+        streams are non-blocking and would not be ordered with it."""
+        if stream == 0:
+            raise ValueError("pass a non-default stream handle (torch.cuda.Stream().cuda_stream) or None")
         o = L.bbtc_ctx_opts(device, ctypes.c_void_p(stream) if stream else None, copy_streams, 0)
         h = ctypes.c_void_p()
         L.check(L.bbtc_ctx_create(ctypes.byref(o), ctypes.byref(h)))

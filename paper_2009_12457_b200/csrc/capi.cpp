@@ -6,6 +6,8 @@
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -14,6 +16,46 @@ namespace bbtc {
 static thread_local std::string t_err;
 void set_error(const std::string& msg) { t_err = msg; }
 [[noreturn]] void raise(bbtc_status code, const std::string& msg) { throw Error{code, msg}; }
+
+static bool trace_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("BBTC_TRACE");
+    on = e && *e && *e != '0';
+  }
+  return on == 1;
+}
+
+Trace::Trace(cudaStream_t s, const char* name) : st(s), phase(name), on(trace_enabled()) { mark("begin"); }
+
+void Trace::mark(const char* what) {
+  if (!on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  ev.emplace_back(what, e);
+}
+
+Trace::~Trace() {
+  if (!on) return;
+  mark("end");
+  cudaEventSynchronize(ev.back().second);
+  std::string line = std::string("[bbtc trace] ") + phase + ":";
+  float total = 0;
+  for (size_t x = 1; x < ev.size(); ++x) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[x - 1].second, ev[x].second);
+    total += ms;
+    char buf[96];
+    snprintf(buf, sizeof buf, " %s=%.3f", ev[x].first, ms);
+    line += buf;
+  }
+  char buf[64];
+  snprintf(buf, sizeof buf, " | total=%.3f ms\n", total);
+  line += buf;
+  fputs(line.c_str(), stderr);
+  for (auto& p : ev) cudaEventDestroy(p.second);
+}
 
 template <class F>
 static bbtc_status guard(F f) {
@@ -30,6 +72,54 @@ static bbtc_status guard(F f) {
     t_err = e.what();
     return BBTC_EINVAL;
   }
+}
+
+// ---- caching allocator ------------------------------------------------------------
+// Size classes: 512 B granules below 4 KiB, else 8 classes per power of two (<= 12.5%
+// waste).  A freed block is reusable by any later allocation on the context stream
+// (stream order makes the reuse safe); beyond cache_limit blocks go back to the pool.
+static size_t size_class(size_t b) {
+  if (b <= 4096) return (b + 511) & ~size_t(511);
+  int lg = 63 - __builtin_clzll(b);
+  size_t step = size_t(1) << (lg - 3);
+  return (b + step - 1) & ~(step - 1);
+}
+
+void* ctx_alloc(bbtc_ctx* ctx, size_t bytes) {
+  const size_t sz = size_class(bytes);
+  auto it = ctx->cache.find(sz);
+  if (it != ctx->cache.end()) {
+    void* p = it->second;
+    ctx->cache.erase(it);
+    ctx->cached_bytes -= sz;
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, sz, ctx->stream);
+  if (e == cudaErrorMemoryAllocation && !ctx->cache.empty()) {
+    cudaGetLastError();
+    for (auto& kv : ctx->cache) cudaFreeAsync(kv.second, ctx->stream);
+    ctx->cache.clear();
+    ctx->cached_bytes = 0;
+    cudaStreamSynchronize(ctx->stream);
+    e = cudaMallocAsync(&p, sz, ctx->stream);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    raise(e == cudaErrorMemoryAllocation ? BBTC_ENOMEM : BBTC_ECUDA,
+          std::string("device allocation of ") + std::to_string(sz) + " bytes: " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void ctx_free(bbtc_ctx* ctx, void* p, size_t bytes) {
+  const size_t sz = size_class(bytes);
+  if (ctx->cached_bytes + sz > ctx->cache_limit) {
+    cudaFreeAsync(p, ctx->stream);
+    return;
+  }
+  ctx->cache.emplace(sz, p);
+  ctx->cached_bytes += sz;
 }
 
 static inline uint64_t C2(uint64_t n) { return n < 2 ? 0 : n * (n - 1) / 2; }
@@ -52,16 +142,24 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   const uint32_t p = plan->p;
   plan->tasks.clear();
   plan->tasks.reserve(n_tasks(p));
-  // Chunk: enough items for ~16 per warp slot on 148 SMs, within [256, 4096].
-  const uint64_t visits_est = [&] {
-    uint64_t v = 0;
-    for (uint32_t j = 0; j < p; ++j)
-      for (uint32_t i = 0; i <= j; ++i) v += plan->blocks[block_id(i, j)].nnz * (p - j);
-    return v;
-  }();
-  uint64_t chunk = visits_est / (148ull * 64 * 16);
-  chunk = std::max<uint64_t>(256, std::min<uint64_t>(4096, (chunk + 31) / 32 * 32));
-  plan->chunk = (uint32_t)chunk;
+  // Work items: each task's G_ij edges are cut into chunks of roughly equal
+  // estimated work, so no warp is left with one heavy item at the end of the launch.
+  // Per-edge cost estimate (the paper's ExecTime density terms):
+  // c(t) = 8 + delta(G_ik) + delta(G_jk), delta(G_ab) = nnz(G_ab) / |V_a|.
+  auto delta = [&](uint32_t b) {
+    const BlockDesc& B = plan->blocks[b];
+    const uint32_t rows = plan->cuts[B.i + 1] - plan->cuts[B.i];
+    return rows ? (double)B.nnz / rows : 0.0;
+  };
+  double work_total = 0;
+  for (uint32_t k = 0; k < p; ++k)
+    for (uint32_t j = 0; j <= k; ++j)
+      for (uint32_t i = 0; i <= j; ++i)
+        work_total += (double)plan->blocks[block_id(i, j)].nnz *
+                      (8.0 + delta(block_id(i, k)) + delta(block_id(j, k)));
+  // ~24 items per warp slot of a full B200 (148 SMs x 40 warps).
+  const double item_work = std::max(1.0, work_total / (148.0 * 40 * 24));
+  plan->chunk = 0;
   plan->item_start.assign(1, 0);
   uint64_t max_task_bytes = 0;
   auto bbytes = [&](uint32_t b) {
@@ -76,6 +174,10 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         T.ik = block_id(i, k);
         T.jk = block_id(j, k);
         T.idx = (uint32_t)task_index(p, i, j, k);
+        const double per_edge = 8.0 + delta(T.ik) + delta(T.jk);
+        uint64_t chunk = (uint64_t)(item_work / per_edge);
+        chunk = std::max<uint64_t>(64, std::min<uint64_t>(1u << 16, (chunk + 31) / 32 * 32));
+        T.chunk = (uint32_t)chunk;
         plan->tasks.push_back(T);
         const uint64_t nnz = plan->blocks[T.ij].nnz;
         plan->item_start.push_back(plan->item_start.back() + (nnz + chunk - 1) / chunk);
@@ -86,8 +188,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   plan->info.work_items = plan->item_start.back();
   plan->info.max_task_bytes = max_task_bytes;
   bbtc_ctx* ctx = plan->ctx;
-  plan->d_tasks.alloc(plan->tasks.size(), ctx->stream);
-  plan->d_item_start.alloc(plan->item_start.size(), ctx->stream);
+  plan->d_tasks.alloc(plan->tasks.size(), ctx);
+  plan->d_item_start.alloc(plan->item_start.size(), ctx);
   BBTC_CUDA(cudaMemcpyAsync(plan->d_tasks.p, plan->tasks.data(), plan->tasks.size() * sizeof(TaskDesc),
                             cudaMemcpyHostToDevice, ctx->stream));
   BBTC_CUDA(cudaMemcpyAsync(plan->d_item_start.p, plan->item_start.data(), plan->item_start.size() * 8,
@@ -143,15 +245,15 @@ static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (!plan->rowptr.p) {
       uint64_t ro = 0;
       for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
-      plan->rowptr.alloc(ro, ctx->stream);
+      plan->rowptr.alloc(ro, ctx);
     }
     return;
   }
   uint64_t ro = 0;
   for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
-  plan->cols.alloc(plan->m, ctx->stream);
-  plan->rows.alloc(plan->m, ctx->stream);
-  plan->rowptr.alloc(ro, ctx->stream);
+  plan->cols.alloc(plan->m, ctx);
+  plan->rows.alloc(plan->m, ctx);
+  plan->rowptr.alloc(ro, ctx);
 }
 
 static uint64_t rowptr_len(const bbtc_plan* plan) {
@@ -204,6 +306,9 @@ BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out) 
     BBTC_CUDA(cudaDeviceGetDefaultMemPool(&pool, o.device));
     uint64_t thr = ~0ull;
     BBTC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    size_t free_b = 0, total_b = 0;
+    BBTC_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    c->cache_limit = total_b / 2;
     *out = c;
   });
 }
@@ -214,6 +319,9 @@ BBTC_API void bbtc_ctx_free(bbtc_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto s : c->copy_streams) cudaStreamDestroy(s);
   if (c->cursor) cudaFree(c->cursor);
+  for (auto& kv : c->cache) cudaFreeAsync(kv.second, c->stream);
+  c->cache.clear();
+  cudaStreamSynchronize(c->stream);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -438,7 +546,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     const uint64_t l0 = ctx->launches;
     const uint64_t nt = plan->info.n_tasks;
     DevBuf<uint64_t> d_counts;
-    d_counts.alloc(nt + 1, ctx->stream);
+    d_counts.alloc(nt + 1, ctx);
     cudaEvent_t k0, k1;
     BBTC_CUDA(cudaEventCreate(&k0));
     BBTC_CUDA(cudaEventCreate(&k1));

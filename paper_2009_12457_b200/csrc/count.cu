@@ -26,8 +26,11 @@ namespace bbtc {
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
-constexpr int kSlab = 1024;          // staged A words per warp (4 KiB)
+constexpr int kTable = 1024;         // per-warp shared words: hash table or sorted slab (4 KiB)
+constexpr int kHashCap = kTable / 4; // staged A words per batch in hash mode (load <= 1/4)
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr size_t kSmemBytes = (size_t)kWarps * (kTable * 4 + 32 * 16);
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 #pragma unroll
@@ -38,19 +41,11 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
   return x;
 }
 
-// Last lane o (0..31) with key[o] <= f, key non-decreasing over lanes, key[0] <= f.
-__device__ __forceinline__ int owner_of(uint32_t key, uint32_t f) {
-  int lo = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1) {
-    uint32_t k = __shfl_sync(kFull, key, lo + step);
-    if (k <= f) lo += step;
-  }
-  return lo;
-}
+__device__ __forceinline__ uint32_t lanemask_le(int lane) { return 0xffffffffu >> (31 - lane); }
+__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 // lower_bound search of w in the sorted list A[0..len): true if present.
-__device__ __forceinline__ bool contains_bounded(const uint32_t* A, uint32_t len, uint32_t w) {
+__device__ __forceinline__ bool contains_sorted(const uint32_t* A, uint32_t len, uint32_t w) {
   uint32_t lo = 0, n = len;
   while (n > 0) {
     uint32_t half = n >> 1;
@@ -60,17 +55,70 @@ __device__ __forceinline__ bool contains_bounded(const uint32_t* A, uint32_t len
   return lo < len && A[lo] == w;
 }
 
+__device__ __forceinline__ uint32_t hbucket(uint32_t key, int shift) { return (key * 0x9E3779B1u) >> shift; }
+
+// Segmented flatten: the warp walks the concatenation of per-lane segments
+// [start, start+len) (start = exclusive prefix of len over lanes) 32 positions at a
+// time.  Non-empty segments are compacted into `pay` (one uint4 payload each); the
+// owner of each position is found with one redux.or of the segment starts falling in
+// the current window plus a popc.  `load(f, P)` fetches the position's word one
+// window ahead of `use(f, P, w)` (software pipelining of the gather).
+template <class Ld, class Use>
+__device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uint32_t start, uint4 payload,
+                                        uint32_t total, Ld load, Use use) {
+  const uint32_t nmask = __ballot_sync(kFull, nonempty);
+  if (nonempty) pay[__popc(nmask & lanemask_lt(lane))] = payload;
+  __syncwarp();
+  if (total == 0) return;
+  uint32_t before = 0;   // segment starts < the next window to be resolved
+  auto owner = [&](uint32_t f0) {
+    const uint32_t d = start - f0;
+    const uint32_t starts = __reduce_or_sync(kFull, (nonempty && d < 32) ? (1u << d) : 0u);
+    const uint32_t idx = before + __popc(starts & lanemask_le(lane)) - 1;
+    before += __popc(starts);
+    return idx;
+  };
+  // Two windows in flight: the gathers of windows f0+32 and f0+64 overlap the
+  // probes of window f0.
+  uint4 P0 = pay[owner(0)], P1 = P0;
+  uint32_t w0 = lane < total ? load(lane, P0) : 0, w1 = 0;
+  if (32 < total) {
+    P1 = pay[owner(32)];
+    if (32 + lane < total) w1 = load(32 + lane, P1);
+  }
+  for (uint32_t f0 = 0; f0 < total; f0 += 32) {
+    uint4 P2 = P1;
+    uint32_t w2 = 0;
+    const uint32_t f2 = f0 + 64 + lane;
+    if (f0 + 64 < total) {
+      P2 = pay[owner(f0 + 64)];
+      if (f2 < total) w2 = load(f2, P2);
+    }
+    if (f0 + lane < total) use(f0 + lane, P0, w0);
+    P0 = P1; w0 = w1;
+    P1 = P2; w1 = w2;
+  }
+  __syncwarp();
+}
+
+// Alg. 5 over work items.  kHash: a batch's staged rows live in one shared hash
+// table of 4-word buckets keyed by (w << 5 | row slot) (needs |V_k| < 2^27);
+// otherwise (and for rows too long for the table) they are staged sorted and
+// searched by binary search.
+template <bool kHash>
 __global__ void __launch_bounds__(kWarps * 32)
 k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ rowptr,
         const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items, uint32_t chunk,
-        uint32_t rank,
-        uint32_t world, unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ counts,
-        uint32_t n_tasks) {
-  __shared__ uint32_t slab[kWarps][kSlab];
+        uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
+        unsigned long long* __restrict__ counts, uint32_t n_tasks) {
+  extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  uint32_t* sA = slab[wid];
+  uint32_t* tab = smem + wid * kTable;
+  uint4* tab4 = reinterpret_cast<uint4*>(tab);
+  uint4* pay = reinterpret_cast<uint4*>(smem + kWarps * kTable) + wid * 32;
+  constexpr uint32_t kCap = kHash ? kHashCap : kTable;
 
   for (;;) {
     unsigned long long it = 0;
@@ -88,8 +136,8 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
     const BlockDesc Bij = blocks[T.ij];
     const BlockDesc Bik = blocks[T.ik];
     const BlockDesc Bjk = blocks[T.jk];
-    const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * chunk;
-    const uint64_t e_end = min(e_begin + chunk, Bij.e0 + Bij.nnz);
+    const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * T.chunk;
+    const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
     const uint32_t* rp_ik = rowptr + Bik.ro;
     const uint32_t* c_ik = cols + Bik.e0;
     const uint32_t* rp_jk = rowptr + Bjk.ro;
@@ -98,6 +146,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
     uint32_t hits = 0;
     uint64_t base = e_begin;
     while (base < e_end) {
+      // ---- 32 edges (u,v) of G_ij: A_u = N(G_ik,u), B_v = N(G_jk,v)
       const uint64_t e = base + lane;
       const bool valid = e < e_end;
       const uint32_t u = valid ? rows[e] : 0xFFFFFFFFu;
@@ -111,59 +160,113 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       }
       const uint32_t uprev = __shfl_up_sync(kFull, u, 1);
       const bool leader = valid && (lane == 0 || u != uprev);
+      const uint32_t lmask = __ballot_sync(kFull, leader);
+      const uint32_t le = lmask & lanemask_le(lane);
+      const int my_leader = le ? 31 - __clz(le) : 0;
+      const uint32_t slot = __popc(lmask & lanemask_lt(my_leader));   // row slot 0..31
       const uint32_t lead_len = leader ? alen : 0;
       const uint32_t incl = warp_incl_scan(lead_len, lane);
-      const uint32_t lmask = __ballot_sync(kFull, leader);
-      const uint32_t le_mask = lmask & (0xffffffffu >> (31 - lane));
-      const int my_leader = le_mask ? 31 - __clz(le_mask) : 0;
       const uint32_t aoff = __shfl_sync(kFull, incl - lead_len, my_leader);
       const uint32_t aend = aoff + alen;
-      const uint32_t fit = __ballot_sync(kFull, valid && aend <= kSlab);
-      int L = __popc(fit);   // lanes [0, L) fit: aend is non-decreasing in the lane
-      bool global_mode = false;
+      int L = __popc(__ballot_sync(kFull, valid && aend <= kCap));   // lanes [0,L) fit
+      // mode: 0 = hash (or sorted slab in the !kHash kernel), 1 = sorted slab, 2 = global
+      int mode = 0;
+      bool dense = false;   // single long row hashed at load <= 1/2
       if (L == 0) {
-        // The first row alone exceeds the slab: handle its edges with A in global memory.
+        // The first row alone exceeds the table: take its edges alone.
         const uint32_t u0 = __shfl_sync(kFull, u, 0);
+        const uint32_t a_first = __shfl_sync(kFull, alen, 0);
         L = __popc(__ballot_sync(kFull, valid && u == u0));
-        global_mode = true;
+        if (kHash && a_first <= 2 * kHashCap) dense = true;
+        else mode = a_first <= kTable ? 1 : 2;
+      } else if (!kHash) {
+        mode = 1;
       }
       const bool in = lane < L;
-      if (!global_mode) {
-        // 1. stage the distinct A_u of lanes [0, L) into the slab
+      int shift = 0;
+      uint32_t bmask = 0;
+      if (mode < 2) {
+        // ---- stage A_u of the distinct rows of lanes [0,L)
         const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
-        const uint32_t akey = in ? aoff : 0xFFFFFFFFu;
-        for (uint32_t f0 = 0; f0 < total_a; f0 += 32) {
-          const uint32_t f = f0 + lane;
-          const int o = owner_of(akey, f);
-          const uint32_t src0 = __shfl_sync(kFull, a0, o);
-          const uint32_t off_o = __shfl_sync(kFull, aoff, o);
-          if (f < total_a) sA[f] = c_ik[src0 + (f - off_o)];
+        if (kHash && mode == 0) {
+          uint32_t nb = 16;
+          while ((dense ? 2 * nb : nb) < total_a) nb <<= 1;
+          bmask = nb - 1;
+          shift = 32 - (__ffs(nb) - 1);
+          for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          __syncwarp();
+          flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, slot, 0), total_a,
+                  [&](uint32_t f, uint4 P) { return c_ik[P.x + (f - P.y)]; },
+                  [&](uint32_t, uint4 P, uint32_t w) {
+                    const uint32_t key = (w << 5) | P.z;
+                    uint32_t h = hbucket(key, shift);
+                    for (;;) {
+                      uint32_t* bk = tab + 4 * h;
+                      if (atomicCAS(bk + 0, kEmpty, key) == kEmpty) break;
+                      if (atomicCAS(bk + 1, kEmpty, key) == kEmpty) break;
+                      if (atomicCAS(bk + 2, kEmpty, key) == kEmpty) break;
+                      if (atomicCAS(bk + 3, kEmpty, key) == kEmpty) break;
+                      h = (h + 1) & bmask;
+                    }
+                  });
+        } else {
+          flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, 0, 0), total_a,
+                  [&](uint32_t f, uint4 P) { return c_ik[P.x + (f - P.y)]; },
+                  [&](uint32_t f, uint4, uint32_t w) { tab[f] = w; });
         }
-        __syncwarp();
       }
-      // 2./3. flattened probes over B_v of lanes [0, L)
+      // ---- probe every w of B_v (lanes [0,L)) against its row's staged A_u
       const uint32_t bl = in ? blen : 0;
-      const uint32_t binc = warp_incl_scan(bl, lane);
-      const uint32_t bexc = in ? binc - bl : 0xFFFFFFFFu;
-      const uint32_t total_b = __shfl_sync(kFull, binc, 31);
-      for (uint32_t f0 = 0; f0 < total_b; f0 += 32) {
-        const uint32_t f = f0 + lane;
-        const int o = owner_of(bexc, f);
-        const uint32_t bstart = __shfl_sync(kFull, b0, o);
-        const uint32_t boff = __shfl_sync(kFull, bexc, o);
-        const uint32_t as = __shfl_sync(kFull, global_mode ? a0 : aoff, o);
-        const uint32_t al = __shfl_sync(kFull, alen, o);
-        if (f < total_b) {
-          const uint32_t w = c_jk[bstart + (f - boff)];
-          const uint32_t* A = global_mode ? c_ik + as : sA + as;
-          hits += contains_bounded(A, al, w);
+      if (kHash && mode == 0) {
+        const uint32_t bx = (uint32_t)Bjk.e0 + b0;   // index of B_v[0] in the cols arena
+        auto probe = [&](uint32_t w, uint32_t sl) -> uint32_t {
+          const uint32_t key = (w << 5) | sl;
+          uint32_t h = hbucket(key, shift);
+          uint4 q = tab4[h];
+          bool hit = (q.x == key) | (q.y == key) | (q.z == key) | (q.w == key);
+          while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at load <= 1/4)
+            h = (h + 1) & bmask;
+            q = tab4[h];
+            hit = (q.x == key) | (q.y == key) | (q.z == key) | (q.w == key);
+          }
+          return hit;
+        };
+        // Phase 1: whole 32-word rounds of the long lists, one list at a time: all
+        // lanes read consecutive words of the same B_v, no owner lookup.
+        uint32_t longs = __ballot_sync(kFull, bl >= 32);
+        while (longs) {
+          const int src = __ffs(longs) - 1;
+          longs &= longs - 1;
+          const uint32_t* B = cols + __shfl_sync(kFull, bx, src) + lane;
+          const uint32_t nfull = __shfl_sync(kFull, bl, src) & ~31u;
+          const uint32_t sl = __shfl_sync(kFull, slot, src);
+          uint32_t off = 0;
+          for (; off + 128 <= nfull; off += 128) {
+            const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
+            hits += probe(w1, sl) + probe(w2, sl) + probe(w3, sl) + probe(w4, sl);
+          }
+          for (; off < nfull; off += 32) hits += probe(B[off], sl);
         }
+        // Phase 2: the remainders (< 32 words per list) flattened across the lanes.
+        const uint32_t rem = bl & 31u;
+        const uint32_t rinc = warp_incl_scan(rem, lane);
+        const uint32_t total_r = __shfl_sync(kFull, rinc, 31);
+        const uint32_t rstart = rinc - rem;
+        flatten(pay, lane, rem > 0, rstart, make_uint4(bx + (bl & ~31u) - rstart, slot, 0, 0), total_r,
+                [&](uint32_t f, uint4 P) { return cols[P.x + f]; },
+                [&](uint32_t, uint4 P, uint32_t w) { hits += probe(w, P.y); });
+      } else {
+        const uint32_t binc = warp_incl_scan(bl, lane);
+        const uint32_t total_b = __shfl_sync(kFull, binc, 31);
+        const uint32_t* A = mode == 2 ? c_ik : tab;
+        flatten(pay, lane, bl > 0, binc - bl, make_uint4(b0, binc - bl, mode == 2 ? a0 : aoff, alen), total_b,
+                [&](uint32_t f, uint4 P) { return c_jk[P.x + (f - P.y)]; },
+                [&](uint32_t, uint4 P, uint32_t w) { hits += contains_sorted(A + P.z, P.w, w); });
       }
-      __syncwarp();
       base += L;
     }
-    // one atomic per warp-item
-    uint32_t s = __reduce_add_sync(kFull, hits);
+    // one atomic pair per warp-item
+    const uint32_t s = __reduce_add_sync(kFull, hits);
     if (lane == 0 && s) {
       atomicAdd(&counts[T.idx], (unsigned long long)s);
       atomicAdd(&counts[n_tasks], (unsigned long long)s);
@@ -230,11 +333,19 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   if (!ctx->cursor) BBTC_CUDA(cudaMalloc((void**)&ctx->cursor, 8 * kCursorSlots));
   unsigned long long* cursor = (unsigned long long*)ctx->cursor + (ctx->cursor_next++ % kCursorSlots);
   BBTC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
-  static int per_sm = 0;
-  if (!per_sm) BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count, kWarps * 32, 0));
-  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm, 1),
+  // Hash keys pack a V_k-local id into 27 bits: every part must be smaller than 2^27.
+  uint32_t max_part = 0;
+  for (uint32_t i = 0; i < plan->p; ++i) max_part = std::max(max_part, plan->cuts[i + 1] - plan->cuts[i]);
+  const bool hash = max_part < (1u << 27);
+  auto kern = hash ? k_count<true> : k_count<false>;
+  static int per_sm[2] = {0, 0};
+  if (!per_sm[hash]) {
+    BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[hash], kern, kWarps * 32, kSmemBytes));
+  }
+  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm[hash], 1),
                                            (my_items + kWarps - 1) / kWarps);
-  k_count<<<(unsigned)grid, kWarps * 32, 0, st>>>(
+  kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
       plan->cols.p, plan->rows.p, plan->rowptr.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, plan->chunk, rank, world, cursor,
       (unsigned long long*)d_counts, (uint32_t)nt);
@@ -247,10 +358,10 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan) {
   const uint32_t nb = (uint32_t)plan->blocks.size();
   DevBuf<unsigned long long> ab, nonempty;
   DevBuf<uint32_t> dmax, rpb;
-  ab.alloc(ne, st);
-  nonempty.alloc(nb, st);
-  dmax.alloc(1, st);
-  rpb.alloc(nb, st);
+  ab.alloc(ne, ctx);
+  nonempty.alloc(nb, ctx);
+  dmax.alloc(1, ctx);
+  rpb.alloc(nb, ctx);
   std::vector<uint32_t> h_rpb(nb);
   uint32_t maxrows = 1;
   for (uint32_t b = 0; b < nb; ++b) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -30,12 +31,18 @@ struct Error {
     (ctx)->launches++;                                                                         \
   } while (0)
 
-// ---- device buffers (stream-ordered pool allocations) -------------------------------
+// ---- device buffers ------------------------------------------------------------------
+// All device scratch and arenas come from the context's caching allocator
+// (ctx_alloc/ctx_free, capi.cpp): freed blocks are kept in size classes and reused
+// in stream order by later steps, so repeated runs never go back to the driver.
+void* ctx_alloc(bbtc_ctx* ctx, size_t bytes);
+void ctx_free(bbtc_ctx* ctx, void* p, size_t bytes);
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  cudaStream_t s = nullptr;
+  bbtc_ctx* c = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
@@ -43,27 +50,37 @@ struct DevBuf {
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       reset();
-      p = o.p; n = o.n; s = o.s;
+      p = o.p; n = o.n; c = o.c;
       o.p = nullptr; o.n = 0;
     }
     return *this;
   }
   ~DevBuf() { reset(); }
-  void alloc(size_t count, cudaStream_t stream) {
+  void alloc(size_t count, bbtc_ctx* ctx) {
     reset();
-    s = stream;
+    c = ctx;
     n = count;
-    if (count) BBTC_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), stream));
+    if (count) p = (T*)ctx_alloc(ctx, count * sizeof(T));
   }
   void reset() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) ctx_free(c, p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }
   size_t bytes() const { return n * sizeof(T); }
 };
 
-struct bbtc_ctx_impl;
+// ---- tracing (BBTC_TRACE=1): CUDA events at named points of a phase, printed to
+// stderr with per-point device time when the phase ends.  Off by default.
+struct Trace {
+  cudaStream_t st = nullptr;
+  const char* phase = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  bool on = false;
+  Trace(cudaStream_t s, const char* name);
+  void mark(const char* what);
+  ~Trace();
+};
 
 }  // namespace bbtc
 
@@ -76,6 +93,9 @@ struct bbtc_ctx {
   int sm_count = 148;
   void* cursor = nullptr;          // device scratch: work-item cursors of the count kernel
   uint64_t cursor_next = 0;
+  std::multimap<size_t, void*> cache;   // caching allocator: size class -> free blocks
+  size_t cached_bytes = 0;
+  size_t cache_limit = 0;
 };
 constexpr int kCursorSlots = 1024;
 
@@ -104,6 +124,8 @@ struct BlockDesc {
 struct TaskDesc {
   uint32_t ij, ik, jk;  // block ids
   uint32_t idx;         // canonical Alg. 4 index
+  uint32_t chunk;       // edges of G_ij per work item
+  uint32_t pad;
 };
 
 struct bbtc_plan {

@@ -36,7 +36,7 @@ void cub_call(bbtc_ctx* ctx, F f) {
   size_t bytes = 0;
   BBTC_CUDA(f((void*)nullptr, bytes));
   DevBuf<uint8_t> tmp;
-  tmp.alloc(std::max<size_t>(bytes, 1), ctx->stream);
+  tmp.alloc(std::max<size_t>(bytes, 1), ctx);
   BBTC_CUDA(f((void*)tmp.p, bytes));
   ctx->launches += 1;
 }
@@ -234,12 +234,13 @@ __global__ void k_row_local(const BlockDesc* __restrict__ blocks, const uint32_t
 void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint, int mem,
                  bbtc_graph* g) {
   cudaStream_t st = ctx->stream;
+  Trace tr(st, "graph_build");
   g->raw = E;
   DevBuf<uint32_t> dmax;
-  dmax.alloc(2, st);
+  dmax.alloc(2, ctx);
   BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
   DevBuf<uint64_t> keys;
-  keys.alloc(E, st);
+  keys.alloc(E, ctx);
   if (E) {
     if (mem == BBTC_MEM_DEVICE) {
       k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, keys.p, dmax.p);
@@ -248,8 +249,8 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
       const uint64_t chunk = 1ull << 25;   // 32 Mi pairs = 256 MiB per chunk
       DevBuf<uint32_t> ds, dd;
-      ds.alloc(std::min(E, 2 * chunk), st);
-      dd.alloc(std::min(E, 2 * chunk), st);
+      ds.alloc(std::min(E, 2 * chunk), ctx);
+      dd.alloc(std::min(E, 2 * chunk), ctx);
       cudaStream_t cs = ctx->copy_streams[0];
       cudaEvent_t ev_copied[2], ev_used[2];
       for (int x = 0; x < 2; ++x) {
@@ -276,6 +277,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       }
     }
   }
+  tr.mark("canon");
   uint32_t max_id = 0;
   BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaStreamSynchronize(st));
@@ -288,18 +290,20 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   DevBuf<uint64_t> ukeys;
   if (E) {
     DevBuf<uint64_t> alt;
-    alt.alloc(E, st);
+    alt.alloc(E, ctx);
     cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, 32 + bid, st);
     });
+    tr.mark("sort1");
     DevBuf<uint64_t>& sorted = db.Current() == keys.p ? keys : alt;
     DevBuf<uint64_t>& other = db.Current() == keys.p ? alt : keys;
     DevBuf<uint64_t> nsel;
-    nsel.alloc(1, st);
+    nsel.alloc(1, ctx);
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceSelect::Unique(t, b, sorted.p, other.p, nsel.p, E, st);
     });
+    tr.mark("unique");
     uint64_t cnt = 0, last = 0;
     BBTC_CUDA(cudaMemcpyAsync(&cnt, nsel.p, 8, cudaMemcpyDeviceToHost, st));
     BBTC_CUDA(cudaStreamSynchronize(st));
@@ -315,19 +319,20 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   g->m = m;
   // Degrees and stable degree rank.
   DevBuf<uint32_t> deg;
-  deg.alloc(n, st);
-  g->deg_sorted.alloc(n, st);
-  g->rank.alloc(n, st);
-  g->okeys.alloc(m, st);
+  deg.alloc(n, ctx);
+  g->deg_sorted.alloc(n, ctx);
+  g->rank.alloc(n, ctx);
+  g->okeys.alloc(m, ctx);
   if (n) {
     BBTC_CUDA(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
     if (m) {
       k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, deg.p);
       BBTC_LAUNCHED(ctx);
     }
+    tr.mark("degree");
     DevBuf<uint32_t> ids, order;
-    ids.alloc(n, st);
-    order.alloc(n, st);
+    ids.alloc(n, ctx);
+    order.alloc(n, ctx);
     k_iota<<<grid_for(ctx, n), kThreads, 0, st>>>(ids.p, n);
     BBTC_LAUNCHED(ctx);
     const int bdeg = std::max(1, bitlen(std::min<uint64_t>(m, n - 1)));
@@ -336,10 +341,12 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     });
     k_rank<<<grid_for(ctx, n), kThreads, 0, st>>>(order.p, n, g->rank.p);
     BBTC_LAUNCHED(ctx);
+    tr.mark("rank");
     if (m) {
       k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, g->rank.p, g->okeys.p);
       BBTC_LAUNCHED(ctx);
     }
+    tr.mark("orient");
     k_graph_stats<<<1, 32, 0, st>>>(g->deg_sorted.p, n, dmax.p);
     BBTC_LAUNCHED(ctx);
     uint32_t h[2];
@@ -355,8 +362,8 @@ void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* 
   std::vector<uint64_t> keys(g->m);
   if (g->m) {
     DevBuf<uint64_t> a, b;
-    a.alloc(g->m, st);
-    b.alloc(g->m, st);
+    a.alloc(g->m, ctx);
+    b.alloc(g->m, ctx);
     BBTC_CUDA(cudaMemcpyAsync(a.p, g->okeys.p, g->m * 8, cudaMemcpyDeviceToDevice, st));
     cub::DoubleBuffer<uint64_t> db(a.p, b.p);
     cub_call(ctx, [&](void* t, size_t& bb) { return cub::DeviceRadixSort::SortKeys(t, bb, db, g->m, 0, 64, st); });
@@ -374,6 +381,7 @@ void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* 
 void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,
                 bbtc_plan* plan) {
   cudaStream_t st = ctx->stream;
+  Trace tr(st, "plan_build");
   const uint32_t n = g->n;
   const uint64_t m = g->m;
   plan->n = n;
@@ -394,44 +402,47 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     plan->cuts[pe] = n;
     if (n > 0 && pe > 1) {
       DevBuf<uint64_t> incl;
-      incl.alloc(n, st);
+      incl.alloc(n, ctx);
       cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(g->deg_sorted.p, ToU64{});
       cub_call(ctx, [&](void* t, size_t& b) {
         return cub::DeviceScan::InclusiveSum(t, b, it, incl.p, (uint64_t)n, st);
       });
       DevBuf<uint32_t> dc;
-      dc.alloc(pe + 1, st);
+      dc.alloc(pe + 1, ctx);
       k_cuts<<<1, 256, 0, st>>>(incl.p, n, 2 * m, pe, dc.p);
       BBTC_LAUNCHED(ctx);
       BBTC_CUDA(cudaMemcpyAsync(plan->cuts.data(), dc.p, (pe + 1) * 4, cudaMemcpyDeviceToHost, st));
       BBTC_CUDA(cudaStreamSynchronize(st));
     }
   }
+  tr.mark("cuts");
   plan->p = pe;
   const uint32_t nb = pe * (pe + 1) / 2;
   const int bn = std::max(1, bitlen(n ? n - 1 : 0));
   const int bp = bitlen(pe - 1);
   if (bp + 2 * bn > 64) raise(BBTC_ERANGE, "n and p too large for the 64-bit block sort key");
   DevBuf<uint32_t> dcuts;
-  dcuts.alloc(pe + 1, st);
+  dcuts.alloc(pe + 1, ctx);
   BBTC_CUDA(cudaMemcpyAsync(dcuts.p, plan->cuts.data(), (pe + 1) * 4, cudaMemcpyHostToDevice, st));
   // ---- a4: block-ordered keys
   DevBuf<uint64_t> ck, ck_alt;
-  ck.alloc(m, st);
+  ck.alloc(m, ctx);
   std::vector<uint64_t> starts(nb + 1, 0);
   const size_t cut_smem = (pe + 1) * 4;
   if (m) {
     k_block_keys<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(g->okeys.p, m, dcuts.p, pe, bn, ck.p);
     BBTC_LAUNCHED(ctx);
-    ck_alt.alloc(m, st);
+    tr.mark("block_keys");
+    ck_alt.alloc(m, ctx);
     cub::DoubleBuffer<uint64_t> db(ck.p, ck_alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, db, m, 0, bp + 2 * bn, st);
     });
     if (db.Current() != ck.p) std::swap(ck, ck_alt);
     ck_alt.reset();
+    tr.mark("sort2");
     DevBuf<uint64_t> dstarts;
-    dstarts.alloc(nb + 1, st);
+    dstarts.alloc(nb + 1, ctx);
     k_block_starts<<<(nb + 1 + 127) / 128, 128, 0, st>>>(ck.p, m, dcuts.p, pe, bn, dstarts.p);
     BBTC_LAUNCHED(ctx);
     BBTC_CUDA(cudaMemcpyAsync(starts.data(), dstarts.p, (nb + 1) * 8, cudaMemcpyDeviceToHost, st));
@@ -453,10 +464,10 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       m_max = std::max(m_max, B.nnz);
       bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1);
     }
-  plan->cols.alloc(m, st);
-  plan->rows.alloc(m, st);
-  plan->rowptr.alloc(ro, st);
-  plan->d_blocks.alloc(nb, st);
+  plan->cols.alloc(m, ctx);
+  plan->rows.alloc(m, ctx);
+  plan->rowptr.alloc(ro, ctx);
+  plan->d_blocks.alloc(nb, ctx);
   BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0xFF, ro * 4, st));
   if (m) {
@@ -464,6 +475,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
                                                           plan->rows.p, plan->rowptr.p);
     BBTC_LAUNCHED(ctx);
   }
+  tr.mark("split");
   ck.reset();
   k_row_ends<<<(nb + 127) / 128, 128, 0, st>>>(plan->d_blocks.p, nb, dcuts.p, plan->rowptr.p);
   BBTC_LAUNCHED(ctx);
@@ -481,6 +493,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     k_row_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dcuts.p, plan->rowptr.p);
     BBTC_LAUNCHED(ctx);
   }
+  tr.mark("rowptr");
   // ---- a5: tasks and work items (host)
   plan->info.p = pe;
   plan->info.clamped = plan->clamped;
@@ -491,6 +504,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   plan->info.lambda = m ? (double)m_max / (2.0 * (double)m / ((double)pe * (pe + 1))) : 0.0;
   plan->info.block_bytes = bytes;
   plan_tasks(plan, 1);
+  tr.mark("tasks");
   if (flags & BBTC_PLAN_STATS) plan_stats(ctx, plan);
 }
 

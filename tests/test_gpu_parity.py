@@ -197,3 +197,14 @@ def test_full_size_configs(ctx, name):
     s, d = cfg.generate(seed=1)
     og = oracle.OracleGraph(s, d, cfg.n_hint)
     check(ctx, s, d, cfg.n_hint, cfg.p, og=og)
+
+
+def test_huge_part_uses_sorted_path(ctx):
+    """A part with >= 2^27 vertices disables the hash keys: the sorted-slab kernel must agree."""
+    s, d = inputs.rmat(14, 16, 3)
+    spread = (s.astype(np.uint64) * 8209 % (1 << 27)).astype(np.uint32), \
+             (d.astype(np.uint64) * 8209 % (1 << 27)).astype(np.uint32)
+    n = (1 << 27) + 5
+    og = oracle.OracleGraph(spread[0], spread[1], n)
+    check(ctx, spread[0], spread[1], n, p=1, og=og)
+    check(ctx, spread[0], spread[1], n, cuts=[0, (1 << 27) + 1, n], og=og)
