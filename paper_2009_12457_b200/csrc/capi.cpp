@@ -213,6 +213,7 @@ struct Streamer {
   std::vector<cudaEvent_t> ev;      // per block: copy finished
   uint64_t bytes = 0;
   uint32_t rr = 0;
+  uint32_t epoch = 0;   // nonzero: flag each block ready on the device after its copy
 
   Streamer(bbtc_ctx* c, bbtc_plan* p) : ctx(c), plan(p), issued(p->blocks.size(), 0), ev(p->blocks.size(), nullptr) {}
   ~Streamer() {
@@ -234,6 +235,12 @@ struct Streamer {
       BBTC_CUDA(cudaMemcpyAsync(plan->rows.p + B.e0, plan->h_rows + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
     }
     BBTC_CUDA(cudaMemcpyAsync(plan->rowptr.p + B.ro, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
+    if (epoch) {
+      // The ready flag is a 4-byte copy from pinned memory queued behind the block's
+      // copies: the copy engine writes it after the data, no SM involved.
+      plan->h_ready[b] = epoch;
+      BBTC_CUDA(cudaMemcpyAsync(plan->d_ready.p + b, plan->h_ready + b, 4, cudaMemcpyHostToDevice, cs));
+    }
     BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     BBTC_CUDA(cudaEventRecord(ev[b], cs));
     bytes += block_bytes(b);
@@ -495,6 +502,7 @@ BBTC_API void bbtc_plan_free(bbtc_plan* plan) {
   if (plan->h_cols) cudaFreeHost(plan->h_cols);
   if (plan->h_rows) cudaFreeHost(plan->h_rows);
   if (plan->h_rowptr) cudaFreeHost(plan->h_rowptr);
+  if (plan->h_ready) cudaFreeHost(plan->h_ready);
   delete plan;
 }
 
@@ -530,7 +538,7 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
     if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
     if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident: call bbtc_stage or bbtc_count");
     count_zero(ctx, plan, d_counts);
-    count_launch(ctx, plan, rank, world, d_counts, 0, plan->item_start.back());
+    count_launch(ctx, plan, rank, world, d_counts, 0, plan->item_start.back(), nullptr, 0);
   });
 }
 
@@ -554,30 +562,36 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     uint64_t h2d = 0;
     BBTC_CUDA(cudaEventRecord(k0, ctx->stream));
     if (plan->resident) {
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back());
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), nullptr, 0);
     } else {
-      // a6: stream blocks in execution order, launching each run of ready tasks.
+      // a6: every block is copied on the copy streams in first-use order and then
+      // flagged ready (epoch) on the device; ONE persistent count kernel runs
+      // concurrently and each warp waits on the flags of its item's three blocks,
+      // so the copies of later tasks overlap the intersections of earlier ones.
       ensure_device_arenas(ctx, plan);
+      if (!plan->d_ready.p) {
+        BBTC_CUDA(cudaHostAlloc((void**)&plan->h_ready, plan->blocks.size() * 4, cudaHostAllocPortable));
+        plan->d_ready.alloc(plan->blocks.size(), ctx);
+        BBTC_CUDA(cudaMemsetAsync(plan->d_ready.p, 0, plan->blocks.size() * 4, ctx->stream));
+      }
+      const uint32_t epoch = ++plan->epoch;
+      // copies may start only after the flag reset above is ordered before them
+      cudaEvent_t go;
+      BBTC_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+      BBTC_CUDA(cudaEventRecord(go, ctx->stream));
+      for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, go, 0));
+      cudaEventDestroy(go);
       Streamer s(ctx, plan);
-      const size_t ne = plan->tasks.size();
-      size_t run0 = 0;
-      auto flush = [&](size_t run1) {
-        if (run1 <= run0) return;
-        for (size_t t = run0; t < run1; ++t)
-          for (uint32_t b : {plan->tasks[t].ij, plan->tasks[t].ik, plan->tasks[t].jk})
-            BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, s.ev[b], 0));
-        count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[run0], plan->item_start[run1]);
-        run0 = run1;
-      };
-      for (size_t t = 0; t < ne; ++t) {
-        const TaskDesc& T = plan->tasks[t];
-        bool fresh = !s.issued[T.ij] || !s.issued[T.ik] || !s.issued[T.jk];
-        if (fresh) flush(t);   // tasks before t only need blocks already issued
+      s.epoch = epoch;
+      for (const TaskDesc& T : plan->tasks) {
         s.issue(T.ij);
         s.issue(T.ik);
         s.issue(T.jk);
       }
-      flush(ne);
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), plan->d_ready.p, epoch);
+      // the count stream must not run past copies it did not wait for
+      for (auto& e : s.ev)
+        if (e) BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
       h2d = s.bytes;
       plan->resident = true;
     }

@@ -111,7 +111,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
         const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items, uint32_t chunk,
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
-        unsigned long long* __restrict__ counts, uint32_t n_tasks) {
+        unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -133,6 +133,23 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const TaskDesc T = tasks[lo];
+    if (ready) {
+      // Streaming (a6): wait until the copy engine has delivered the task's blocks.
+      if (lane == 0) {
+        for (uint32_t b : {T.ij, T.ik, T.jk}) {
+          uint32_t v;
+          uint64_t spins = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + b) : "memory");
+            if (v != epoch) {
+              __nanosleep(1000);
+              if (++spins > (1ull << 25)) __trap();   // ~30 s without the copy: fail, never hang
+            }
+          } while (v != epoch);
+        }
+      }
+      __syncwarp();
+    }
     const BlockDesc Bij = blocks[T.ij];
     const BlockDesc Bik = blocks[T.ik];
     const BlockDesc Bjk = blocks[T.jk];
@@ -325,7 +342,7 @@ void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts) {
 // Enqueues the count kernel over work items [item_lo, item_hi) of the plan's
 // execution order (this rank's residues only), accumulating into d_counts.
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
-                  uint64_t item_lo, uint64_t item_hi) {
+                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch) {
   cudaStream_t st = ctx->stream;
   const uint64_t nt = plan->info.n_tasks;
   if (item_hi <= item_lo + rank) return;
@@ -348,7 +365,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
       plan->cols.p, plan->rows.p, plan->rowptr.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, plan->chunk, rank, world, cursor,
-      (unsigned long long*)d_counts, (uint32_t)nt);
+      (unsigned long long*)d_counts, (uint32_t)nt, ready, epoch);
   BBTC_LAUNCHED(ctx);
 }
 

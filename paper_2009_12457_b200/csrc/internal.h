@@ -146,6 +146,9 @@ struct bbtc_plan {
   bbtc::DevBuf<BlockDesc> d_blocks;
   bbtc::DevBuf<TaskDesc> d_tasks;
   bbtc::DevBuf<uint64_t> d_item_start;
+  bbtc::DevBuf<uint32_t> d_ready;     // streaming: per-block ready epoch
+  uint32_t* h_ready = nullptr;        // pinned source of the ready flags
+  uint32_t epoch = 0;
   // pinned host copies (bbtc_plan_to_host)
   bool host_blocks = false;
   uint32_t* h_cols = nullptr;
@@ -165,7 +168,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
 // count.cu
 void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
-                  uint64_t item_lo, uint64_t item_hi);
+                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
 // capi.cpp (host)
 uint64_t n_tasks(uint32_t p);

@@ -190,7 +190,7 @@ def test_device_input_streaming_and_ranks(ctx):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["orkut", "rmat24"])
+@pytest.mark.parametrize("name", ["orkut", "rmat24", "friendster"])
 def test_full_size_configs(ctx, name):
     """BASELINE.json configs 3 and 4 at full size, whole-result parity with the oracle."""
     cfg = inputs.CONFIGS[name]
