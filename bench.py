@@ -197,6 +197,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2009_12457_b200 as bb
+    from paper_2009_12457_b200.dist import count_distributed, max_over_ranks, reduce_counts
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -233,8 +234,7 @@ def main():
         a.record(stream)
         plan.count_async(counts, rank, world)
         b.record(stream)
-        if world > 1:
-            dist.all_reduce(counts)
+        reduce_counts(counts)
         tot = int(counts[-1].item())
         if record:
             kern_ms.append(a.elapsed_time(b))
@@ -262,9 +262,7 @@ def main():
     ms = s0.elapsed_time(s1) / args.steps
     if world > 1:
         dist.barrier()
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, device="cuda")
     m = st["m"]
     value = m / (ms / 1e3)
     kern = statistics.mean(kern_ms)
@@ -279,9 +277,7 @@ def main():
         a.record(stream)
         g = bb.Graph.from_edges(ctx, hs, hd, cfg.n_hint)
         plan = bb.Plan(ctx, g, p)
-        plan.count_async(counts, rank, world)
-        if world > 1:
-            dist.all_reduce(counts)
+        count_distributed(plan, counts)
         host_counts = counts.cpu()
         b.record(stream)
         torch.cuda.synchronize()
@@ -290,11 +286,7 @@ def main():
         g.close()
         if x:
             e2e_ms.append(a.elapsed_time(b))
-    e2e = statistics.median(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
+    e2e = max_over_ranks(statistics.median(e2e_ms), device="cuda")
 
     # The paper's split (one plan, stats on): count with blocks resident vs streamed.
     g = bb.Graph.from_edges(ctx, ds, dd, cfg.n_hint)

@@ -75,9 +75,9 @@ class Context:
         return int(L.bbtc_ctx_launches(self._h))
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None and L.lib is not None:
             L.bbtc_ctx_free(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()
@@ -126,9 +126,9 @@ class Graph:
         return row, col
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None and L.lib is not None:
             L.bbtc_graph_free(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()
@@ -206,9 +206,9 @@ class Plan:
         L.check(L.bbtc_count_async(self.ctx.handle, self._h, rank, world, ctypes.c_void_p(d_counts.data_ptr())))
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None and L.lib is not None:
             L.bbtc_plan_free(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()

@@ -42,22 +42,24 @@ void cub_call(bbtc_ctx* ctx, F f) {
 }
 
 // ---- a1 ------------------------------------------------------------------------------
-// key = (min << 32) | max for a != b, kSentinel for self-loops; tracks the largest id.
-__global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t E,
+// key = (min << bw) | max for a != b, kSentinel for self-loops; tracks the largest id.
+// bw is the id width guessed from n_hint (32 when unknown); graph_build re-runs with
+// bw = 32 if an id does not fit.  Narrow keys save radix-sort passes.
+__global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t E, int bw,
                         uint64_t* __restrict__ keys, uint32_t* __restrict__ max_id) {
   uint32_t mx = 0;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t a = src[e], b = dst[e];
     uint32_t lo = min(a, b), hi = max(a, b);
     mx = max(mx, hi);
-    keys[e] = a == b ? kSentinel : ((uint64_t)lo << 32) | hi;
+    keys[e] = a == b ? kSentinel : ((uint64_t)lo << bw) | hi;
   }
   mx = __reduce_max_sync(0xffffffffu, mx);
   if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
 }
 
 // ---- a2 ------------------------------------------------------------------------------
-__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ deg) {
+__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, int bw, uint32_t* __restrict__ deg) {
   // Warp-uniform trip count so the whole warp stays converged for __match_any_sync.
   const uint64_t lane = threadIdx.x & 31;
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane;
@@ -66,7 +68,8 @@ __global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, uint32_t
     const uint64_t e = base + lane;
     const bool valid = e < m;
     const uint64_t k = valid ? keys[e] : 0;
-    const uint32_t lo = valid ? (uint32_t)(k >> 32) : 0xFFFFFFFFu, hi = (uint32_t)k;
+    const uint32_t lo = valid ? (uint32_t)(k >> bw) : 0xFFFFFFFFu;
+    const uint32_t hi = (uint32_t)(k & ((1ull << bw) - 1));
     // Keys are sorted, so equal `lo` values sit in the same warp: aggregate them.
     const uint32_t peers = __match_any_sync(0xffffffffu, lo);
     if (valid && lane == (uint64_t)(__ffs(peers) - 1)) atomicAdd(&deg[lo], __popc(peers));
@@ -83,11 +86,11 @@ __global__ void k_rank(const uint32_t* __restrict__ order, uint32_t n, uint32_t*
 }
 
 // Orientation from lower to higher degree rank (P:226-235 with the order of P:438-446).
-__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, const uint32_t* __restrict__ rank,
+__global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, int bw, const uint32_t* __restrict__ rank,
                          uint64_t* __restrict__ okeys) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[e];
-    uint32_t ra = rank[(uint32_t)(k >> 32)], rb = rank[(uint32_t)k];
+    uint32_t ra = rank[(uint32_t)(k >> bw)], rb = rank[(uint32_t)(k & ((1ull << bw) - 1))];
     okeys[e] = ((uint64_t)min(ra, rb) << 32) | max(ra, rb);
   }
 }
@@ -241,51 +244,62 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
   DevBuf<uint64_t> keys;
   keys.alloc(E, ctx);
-  if (E) {
+  int bw = n_hint > 1 ? std::max(1, bitlen(n_hint - 1)) : 32;
+  auto canon = [&](int width) {
+    BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
+    if (!E) return;
     if (mem == BBTC_MEM_DEVICE) {
-      k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, keys.p, dmax.p);
+      k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, width, keys.p, dmax.p);
       BBTC_LAUNCHED(ctx);
-    } else {
-      // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
-      const uint64_t chunk = 1ull << 25;   // 32 Mi pairs = 256 MiB per chunk
-      DevBuf<uint32_t> ds, dd;
-      ds.alloc(std::min(E, 2 * chunk), ctx);
-      dd.alloc(std::min(E, 2 * chunk), ctx);
-      cudaStream_t cs = ctx->copy_streams[0];
-      cudaEvent_t ev_copied[2], ev_used[2];
-      for (int x = 0; x < 2; ++x) {
-        BBTC_CUDA(cudaEventCreateWithFlags(&ev_copied[x], cudaEventDisableTiming));
-        BBTC_CUDA(cudaEventCreateWithFlags(&ev_used[x], cudaEventDisableTiming));
-        BBTC_CUDA(cudaEventRecord(ev_used[x], st));
-      }
-      for (uint64_t c0 = 0, it = 0; c0 < E; c0 += chunk, ++it) {
-        const uint64_t len = std::min(chunk, E - c0);
-        const int slot = it & 1;
-        BBTC_CUDA(cudaStreamWaitEvent(cs, ev_used[slot], 0));
-        BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
-        BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
-        BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
-        BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
-        k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(ds.p + slot * chunk, dd.p + slot * chunk, len, keys.p + c0,
-                                                          dmax.p);
-        BBTC_LAUNCHED(ctx);
-        BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
-      }
-      for (int x = 0; x < 2; ++x) {
-        cudaEventDestroy(ev_copied[x]);
-        cudaEventDestroy(ev_used[x]);
-      }
+      return;
     }
-  }
+    // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
+    const uint64_t chunk = 1ull << 25;   // 32 Mi pairs = 256 MiB per chunk
+    DevBuf<uint32_t> ds, dd;
+    ds.alloc(std::min(E, 2 * chunk), ctx);
+    dd.alloc(std::min(E, 2 * chunk), ctx);
+    cudaStream_t cs = ctx->copy_streams[0];
+    cudaEvent_t ev_copied[2], ev_used[2];
+    for (int x = 0; x < 2; ++x) {
+      BBTC_CUDA(cudaEventCreateWithFlags(&ev_copied[x], cudaEventDisableTiming));
+      BBTC_CUDA(cudaEventCreateWithFlags(&ev_used[x], cudaEventDisableTiming));
+      BBTC_CUDA(cudaEventRecord(ev_used[x], st));
+    }
+    for (uint64_t c0 = 0, it = 0; c0 < E; c0 += chunk, ++it) {
+      const uint64_t len = std::min(chunk, E - c0);
+      const int slot = it & 1;
+      BBTC_CUDA(cudaStreamWaitEvent(cs, ev_used[slot], 0));
+      BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
+      BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
+      BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
+      BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
+      k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(ds.p + slot * chunk, dd.p + slot * chunk, len, width,
+                                                        keys.p + c0, dmax.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
+    }
+    for (int x = 0; x < 2; ++x) {
+      cudaEventDestroy(ev_copied[x]);
+      cudaEventDestroy(ev_used[x]);
+    }
+  };
+  canon(bw);
   tr.mark("canon");
   uint32_t max_id = 0;
   BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaStreamSynchronize(st));
+  if (E && bw < 32 && (max_id >> bw) != 0) {
+    // n_hint was too small for the ids: rebuild the keys at full width.
+    bw = 32;
+    canon(bw);
+    BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  }
   if (E && max_id == 0xFFFFFFFFu) raise(BBTC_ERANGE, "vertex id 0xFFFFFFFF is reserved");
   const uint32_t n = E ? std::max<uint32_t>(n_hint, max_id + 1) : n_hint;
   g->n = n;
   const int bid = std::max(1, bitlen(max_id));
-  // Sort the canonical keys over their live bits (hi id in [0,bid), lo id in [32,32+bid)).
+  // Sort the canonical keys over their live bits (hi id in [0,bid), lo id in [bw,bw+bid)).
   uint64_t m = 0;
   DevBuf<uint64_t> ukeys;
   if (E) {
@@ -293,7 +307,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     alt.alloc(E, ctx);
     cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, 32 + bid, st);
+      return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, bw + bid, st);
     });
     tr.mark("sort1");
     DevBuf<uint64_t>& sorted = db.Current() == keys.p ? keys : alt;
@@ -326,7 +340,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   if (n) {
     BBTC_CUDA(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
     if (m) {
-      k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, deg.p);
+      k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
       BBTC_LAUNCHED(ctx);
     }
     tr.mark("degree");
@@ -343,7 +357,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     BBTC_LAUNCHED(ctx);
     tr.mark("rank");
     if (m) {
-      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, g->rank.p, g->okeys.p);
+      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, g->rank.p, g->okeys.p);
       BBTC_LAUNCHED(ctx);
     }
     tr.mark("orient");

@@ -208,3 +208,11 @@ def test_huge_part_uses_sorted_path(ctx):
     og = oracle.OracleGraph(spread[0], spread[1], n)
     check(ctx, spread[0], spread[1], n, p=1, og=og)
     check(ctx, spread[0], spread[1], n, cuts=[0, (1 << 27) + 1, n], og=og)
+
+
+@pytest.mark.parametrize("n_hint", [0, 1, 5, 1000, 1 << 20])
+def test_n_hint_does_not_matter_except_isolated(ctx, n_hint):
+    """Narrow sort keys are sized from n_hint; a wrong hint must not change results."""
+    s, d = inputs.rmat(10, 16, 7)
+    og = oracle.OracleGraph(s, d, n_hint)
+    check(ctx, s, d, n_hint, p=3, og=og)
