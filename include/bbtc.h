@@ -125,9 +125,13 @@ typedef struct {
                                BBTC_PLAN_STATS was passed */
   uint64_t visits;          /* edge visits summed over tasks, i.e. sum_t nnz(G_ij); ditto */
   uint64_t work_items;      /* work items the count kernel schedules */
+  uint64_t sum_a;           /* Σ_t Σ_(u,v)∈G_ij d(G_ik,u) (BBTC_PLAN_STATS) */
+  uint64_t sum_b;           /* Σ_t Σ_(u,v)∈G_ij d(G_jk,v) (BBTC_PLAN_STATS) */
 } bbtc_plan_info;
 
-#define BBTC_PLAN_STATS 1u   /* compute b_alg / visits / dmax_blk (one extra device pass) */
+#define BBTC_PLAN_STATS 1u     /* compute b_alg / visits / dmax_blk (one extra device pass) */
+#define BBTC_PLAN_ROWMAJOR 2u  /* walk G_ij row by row (stage N(G_ik,u), gather N(G_jk,v)) instead of
+                                  the default column order (stage N(G_jk,v), gather N(G_ik,u)) */
 
 /* a3-a5.  p: requested parts (>= 1; clamped to n).  cuts: NULL for the default
  * rule (R5: full-degree prefix rule) or a host array of p+1 entries

@@ -169,6 +169,6 @@ CONFIGS = {
     "orkut": Config("orkut", "chunglu", p=8, n=3_072_441, m=117_185_083, gamma=2.3314, dmax=33_313,
                     desc="com-Orkut-shaped Chung-Lu, 8x8 blocks"),
     "rmat24": Config("rmat24", "rmat", p=16, scale=24, desc="R-MAT scale 24 ef 16, 16x16 blocks"),
-    "friendster": Config("friendster", "chunglu", p=16, n=65_608_366, m=1_806_067_135, gamma=2.0,
-                         dmax=5_214, desc="Friendster-shaped Chung-Lu, 16x16 blocks"),
+    "friendster": Config("friendster", "chunglu", p=4, n=65_608_366, m=1_806_067_135, gamma=2.0,
+                         dmax=5_214, desc="Friendster-shaped Chung-Lu, 4x4 blocks"),
 }

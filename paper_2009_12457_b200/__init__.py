@@ -137,7 +137,10 @@ class Graph:
 class Plan:
     """Cut vector + BCSR blocks + task list (bbtc_plan)."""
 
-    def __init__(self, ctx: Context, graph: Graph, p: int = 1, cuts=None, stats: bool = False):
+    def __init__(self, ctx: Context, graph: Graph, p: int = 1, cuts=None, stats: bool = False,
+                 row_major: bool = False):
+        """row_major: walk each G_ij row by row (stage N(G_ik,u), gather N(G_jk,v)) instead of the
+        default column order (stage N(G_jk,v), gather N(G_ik,u)).  Same counts either way."""
         self.ctx = ctx
         h = ctypes.c_void_p()
         cptr = None
@@ -145,7 +148,8 @@ class Plan:
             self._cuts_in = np.ascontiguousarray(cuts, dtype=np.uint32)
             p = len(self._cuts_in) - 1
             cptr = self._cuts_in.ctypes.data_as(L._u32p)
-        L.check(L.bbtc_plan_create(ctx.handle, graph._h, p, cptr, PLAN_STATS if stats else 0, ctypes.byref(h)))
+        flags = (L.PLAN_STATS if stats else 0) | (L.PLAN_ROWMAJOR if row_major else 0)
+        L.check(L.bbtc_plan_create(ctx.handle, graph._h, p, cptr, flags, ctypes.byref(h)))
         self._h = h
 
     def info(self) -> dict:

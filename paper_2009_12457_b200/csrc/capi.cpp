@@ -222,7 +222,7 @@ struct Streamer {
   }
   uint64_t block_bytes(uint32_t b) const {
     const BlockDesc& B = plan->blocks[b];
-    return 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+    return 4 * B.nnz * plan->edge_arenas().size() + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
   }
   void issue(uint32_t b) {
     if (issued[b]) return;
@@ -230,10 +230,9 @@ struct Streamer {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
-    if (B.nnz) {
-      BBTC_CUDA(cudaMemcpyAsync(plan->cols.p + B.e0, plan->h_cols + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
-      BBTC_CUDA(cudaMemcpyAsync(plan->rows.p + B.e0, plan->h_rows + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
-    }
+    if (B.nnz)
+      for (auto& A : plan->edge_arenas())
+        BBTC_CUDA(cudaMemcpyAsync(A.dev->p + B.e0, *A.host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
     BBTC_CUDA(cudaMemcpyAsync(plan->rowptr.p + B.ro, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
     if (epoch) {
       // The ready flag is a 4-byte copy from pinned memory queued behind the block's
@@ -247,26 +246,16 @@ struct Streamer {
   }
 };
 
-static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
-  if (plan->cols.p || plan->m == 0) {
-    if (!plan->rowptr.p) {
-      uint64_t ro = 0;
-      for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
-      plan->rowptr.alloc(ro, ctx);
-    }
-    return;
-  }
-  uint64_t ro = 0;
-  for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
-  plan->cols.alloc(plan->m, ctx);
-  plan->rows.alloc(plan->m, ctx);
-  plan->rowptr.alloc(ro, ctx);
-}
-
 static uint64_t rowptr_len(const bbtc_plan* plan) {
   uint64_t ro = 0;
   for (auto& B : plan->blocks) ro += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
   return ro;
+}
+
+static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (!plan->rowptr.p) plan->rowptr.alloc(rowptr_len(plan), ctx);
+  for (auto& A : plan->edge_arenas())
+    if (!A.dev->p && plan->m) A.dev->alloc(plan->m, ctx);
 }
 
 }  // namespace bbtc
@@ -435,16 +424,19 @@ BBTC_API bbtc_status bbtc_plan_block(bbtc_ctx* ctx, const bbtc_plan* plan, uint3
     if (nnz) *nnz = B.nnz;
     const uint64_t rlen = (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
     cudaStream_t st = ctx->stream;
+    std::vector<uint32_t> rp(rlen);
     if (plan->host_blocks && !plan->resident) {
-      if (row_ptr) std::memcpy(row_ptr, plan->h_rowptr + B.ro, rlen * 4);
+      std::memcpy(rp.data(), plan->h_rowptr + B.ro, rlen * 4);
       if (col) std::memcpy(col, plan->h_cols + B.e0, B.nnz * 4);
-      if (row) std::memcpy(row, plan->h_rows + B.e0, B.nnz * 4);
-      return;
+    } else {
+      BBTC_CUDA(cudaMemcpyAsync(rp.data(), plan->rowptr.p + B.ro, rlen * 4, cudaMemcpyDeviceToHost, st));
+      if (col && B.nnz) BBTC_CUDA(cudaMemcpyAsync(col, plan->cols.p + B.e0, B.nnz * 4, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaStreamSynchronize(st));
     }
-    if (row_ptr) BBTC_CUDA(cudaMemcpyAsync(row_ptr, plan->rowptr.p + B.ro, rlen * 4, cudaMemcpyDeviceToHost, st));
-    if (col && B.nnz) BBTC_CUDA(cudaMemcpyAsync(col, plan->cols.p + B.e0, B.nnz * 4, cudaMemcpyDeviceToHost, st));
-    if (row && B.nnz) BBTC_CUDA(cudaMemcpyAsync(row, plan->rows.p + B.e0, B.nnz * 4, cudaMemcpyDeviceToHost, st));
-    BBTC_CUDA(cudaStreamSynchronize(st));
+    if (row_ptr) std::copy(rp.begin(), rp.end(), row_ptr);
+    if (row)   // the row id of every edge, expanded from the row offsets
+      for (uint64_t r = 0; r + 1 < rlen; ++r)
+        for (uint32_t x = rp[r]; x < rp[r + 1]; ++x) row[x] = (uint32_t)r;
   });
 }
 
@@ -453,18 +445,15 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
     if (plan->host_blocks) return;
     const uint64_t ro = rowptr_len(plan);
-    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_cols, std::max<uint64_t>(plan->m, 1) * 4, cudaHostAllocPortable));
-    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rows, std::max<uint64_t>(plan->m, 1) * 4, cudaHostAllocPortable));
-    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rowptr, std::max<uint64_t>(ro, 1) * 4, cudaHostAllocPortable));
     cudaStream_t st = ctx->stream;
-    if (plan->m) {
-      BBTC_CUDA(cudaMemcpyAsync(plan->h_cols, plan->cols.p, plan->m * 4, cudaMemcpyDeviceToHost, st));
-      BBTC_CUDA(cudaMemcpyAsync(plan->h_rows, plan->rows.p, plan->m * 4, cudaMemcpyDeviceToHost, st));
+    for (auto& A : plan->edge_arenas()) {
+      BBTC_CUDA(cudaHostAlloc((void**)A.host, std::max<uint64_t>(plan->m, 1) * 4, cudaHostAllocPortable));
+      if (plan->m) BBTC_CUDA(cudaMemcpyAsync(*A.host, A.dev->p, plan->m * 4, cudaMemcpyDeviceToHost, st));
     }
+    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rowptr, std::max<uint64_t>(ro, 1) * 4, cudaHostAllocPortable));
     BBTC_CUDA(cudaMemcpyAsync(plan->h_rowptr, plan->rowptr.p, ro * 4, cudaMemcpyDeviceToHost, st));
     BBTC_CUDA(cudaStreamSynchronize(st));
-    plan->cols.reset();
-    plan->rows.reset();
+    for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
     plan->host_blocks = true;
     plan->resident = false;
@@ -489,8 +478,7 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
     if (!plan->host_blocks) return;   // device plans own their only copy
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
-    plan->cols.reset();
-    plan->rows.reset();
+    for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
     plan->resident = false;
   });
@@ -501,6 +489,8 @@ BBTC_API void bbtc_plan_free(bbtc_plan* plan) {
   if (plan->ctx) cudaStreamSynchronize(plan->ctx->stream);
   if (plan->h_cols) cudaFreeHost(plan->h_cols);
   if (plan->h_rows) cudaFreeHost(plan->h_rows);
+  if (plan->h_ccu) cudaFreeHost(plan->h_ccu);
+  if (plan->h_ccv) cudaFreeHost(plan->h_ccv);
   if (plan->h_rowptr) cudaFreeHost(plan->h_rowptr);
   if (plan->h_ready) cudaFreeHost(plan->h_ready);
   delete plan;

@@ -101,15 +101,19 @@ __device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uin
   __syncwarp();
 }
 
-// Alg. 5 over work items.  kHash: a batch's staged rows live in one shared hash
-// table of 4-word buckets keyed by (w << 5 | row slot) (needs |V_k| < 2^27);
-// otherwise (and for rows too long for the table) they are staged sorted and
-// searched by binary search.
-template <bool kHash>
+// Alg. 5 over work items.  Each edge (u,v) of G_ij needs |N(G_ik,u) ∩ N(G_jk,v)|.
+// The edges of a batch are consecutive in the block's iteration order, so one of
+// the two lists repeats across neighbouring lanes: the "staged" list S (N(G_jk,v)
+// when walking by column, kCol; N(G_ik,u) when walking by row) is put in shared
+// memory once per distinct key, and every word of the other, "probe" list P is
+// looked up in it.  kHash: staged lists share one hash table of 4-word buckets
+// keyed by (w << 5 | slot) (needs |V_k| < 2^27); otherwise (and for lists too long
+// for the table) they are staged sorted and searched by binary search.
+template <bool kHash, bool kCol>
 __global__ void __launch_bounds__(kWarps * 32)
-k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ rowptr,
-        const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
-        const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items, uint32_t chunk,
+k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
+        const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
+        const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
         unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -137,50 +141,52 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       // Streaming (a6): wait until the copy engine has delivered the task's blocks.
       if (lane == 0) {
         for (uint32_t b : {T.ij, T.ik, T.jk}) {
-          uint32_t v;
+          uint32_t rv;
           uint64_t spins = 0;
           do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready + b) : "memory");
-            if (v != epoch) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(rv) : "l"(ready + b) : "memory");
+            if (rv != epoch) {
               __nanosleep(1000);
               if (++spins > (1ull << 25)) __trap();   // ~30 s without the copy: fail, never hang
             }
-          } while (v != epoch);
+          } while (rv != epoch);
         }
       }
       __syncwarp();
     }
     const BlockDesc Bij = blocks[T.ij];
-    const BlockDesc Bik = blocks[T.ik];
-    const BlockDesc Bjk = blocks[T.jk];
+    const BlockDesc BS = blocks[kCol ? T.jk : T.ik];   // block of the staged lists
+    const BlockDesc BP = blocks[kCol ? T.ik : T.jk];   // block of the probe lists
     const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * T.chunk;
     const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
-    const uint32_t* rp_ik = rowptr + Bik.ro;
-    const uint32_t* c_ik = cols + Bik.e0;
-    const uint32_t* rp_jk = rowptr + Bjk.ro;
-    const uint32_t* c_jk = cols + Bjk.e0;
+    const uint32_t* rpS = rowptr + BS.ro;
+    const uint32_t* cS = cols + BS.e0;
+    const uint32_t* rpP = rowptr + BP.ro;
+    const uint32_t* cP = cols + BP.e0;
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
     while (base < e_end) {
-      // ---- 32 edges (u,v) of G_ij: A_u = N(G_ik,u), B_v = N(G_jk,v)
+      // ---- 32 edges (u,v) of G_ij; key = the staged side's row (v by column, u by row)
       const uint64_t e = base + lane;
       const bool valid = e < e_end;
-      const uint32_t u = valid ? rows[e] : 0xFFFFFFFFu;
-      const uint32_t v = valid ? cols[e] : 0;
-      uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;
+      const uint32_t u = valid ? it_u[e] : 0xFFFFFFFFu;
+      const uint32_t v = valid ? it_v[e] : 0xFFFFFFFFu;
+      const uint32_t key = kCol ? v : u;
+      const uint32_t pid = kCol ? u : v;
+      uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;   // a: staged list, b: probe list
       if (valid) {
-        a0 = rp_ik[u];
-        alen = rp_ik[u + 1] - a0;
-        b0 = rp_jk[v];
-        blen = rp_jk[v + 1] - b0;
+        a0 = rpS[key];
+        alen = rpS[key + 1] - a0;
+        b0 = rpP[pid];
+        blen = rpP[pid + 1] - b0;
       }
-      const uint32_t uprev = __shfl_up_sync(kFull, u, 1);
-      const bool leader = valid && (lane == 0 || u != uprev);
+      const uint32_t kprev = __shfl_up_sync(kFull, key, 1);
+      const bool leader = valid && (lane == 0 || key != kprev);
       const uint32_t lmask = __ballot_sync(kFull, leader);
       const uint32_t le = lmask & lanemask_le(lane);
       const int my_leader = le ? 31 - __clz(le) : 0;
-      const uint32_t slot = __popc(lmask & lanemask_lt(my_leader));   // row slot 0..31
+      const uint32_t slot = __popc(lmask & lanemask_lt(my_leader));   // staged-list slot 0..31
       const uint32_t lead_len = leader ? alen : 0;
       const uint32_t incl = warp_incl_scan(lead_len, lane);
       const uint32_t aoff = __shfl_sync(kFull, incl - lead_len, my_leader);
@@ -188,12 +194,12 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       int L = __popc(__ballot_sync(kFull, valid && aend <= kCap));   // lanes [0,L) fit
       // mode: 0 = hash (or sorted slab in the !kHash kernel), 1 = sorted slab, 2 = global
       int mode = 0;
-      bool dense = false;   // single long row hashed at load <= 1/2
+      bool dense = false;   // single long list hashed at load <= 1/2
       if (L == 0) {
-        // The first row alone exceeds the table: take its edges alone.
-        const uint32_t u0 = __shfl_sync(kFull, u, 0);
+        // The first staged list alone exceeds the table: take its edges alone.
+        const uint32_t k0 = __shfl_sync(kFull, key, 0);
         const uint32_t a_first = __shfl_sync(kFull, alen, 0);
-        L = __popc(__ballot_sync(kFull, valid && u == u0));
+        L = __popc(__ballot_sync(kFull, valid && key == k0));
         if (kHash && a_first <= 2 * kHashCap) dense = true;
         else mode = a_first <= kTable ? 1 : 2;
       } else if (!kHash) {
@@ -203,7 +209,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       int shift = 0;
       uint32_t bmask = 0;
       if (mode < 2) {
-        // ---- stage A_u of the distinct rows of lanes [0,L)
+        // ---- stage the distinct lists S of lanes [0,L)
         const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
         if (kHash && mode == 0) {
           uint32_t nb = 16;
@@ -213,43 +219,43 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, slot, 0), total_a,
-                  [&](uint32_t f, uint4 P) { return c_ik[P.x + (f - P.y)]; },
+                  [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
                   [&](uint32_t, uint4 P, uint32_t w) {
-                    const uint32_t key = (w << 5) | P.z;
-                    uint32_t h = hbucket(key, shift);
+                    const uint32_t hk = (w << 5) | P.z;
+                    uint32_t h = hbucket(hk, shift);
                     for (;;) {
                       uint32_t* bk = tab + 4 * h;
-                      if (atomicCAS(bk + 0, kEmpty, key) == kEmpty) break;
-                      if (atomicCAS(bk + 1, kEmpty, key) == kEmpty) break;
-                      if (atomicCAS(bk + 2, kEmpty, key) == kEmpty) break;
-                      if (atomicCAS(bk + 3, kEmpty, key) == kEmpty) break;
+                      if (atomicCAS(bk + 0, kEmpty, hk) == kEmpty) break;
+                      if (atomicCAS(bk + 1, kEmpty, hk) == kEmpty) break;
+                      if (atomicCAS(bk + 2, kEmpty, hk) == kEmpty) break;
+                      if (atomicCAS(bk + 3, kEmpty, hk) == kEmpty) break;
                       h = (h + 1) & bmask;
                     }
                   });
         } else {
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, 0, 0), total_a,
-                  [&](uint32_t f, uint4 P) { return c_ik[P.x + (f - P.y)]; },
+                  [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
                   [&](uint32_t f, uint4, uint32_t w) { tab[f] = w; });
         }
       }
-      // ---- probe every w of B_v (lanes [0,L)) against its row's staged A_u
+      // ---- probe every word w of each lane's list P against its staged list
       const uint32_t bl = in ? blen : 0;
       if (kHash && mode == 0) {
-        const uint32_t bx = (uint32_t)Bjk.e0 + b0;   // index of B_v[0] in the cols arena
+        const uint32_t bx = (uint32_t)BP.e0 + b0;   // index of P[0] in the cols arena
         auto probe = [&](uint32_t w, uint32_t sl) -> uint32_t {
-          const uint32_t key = (w << 5) | sl;
-          uint32_t h = hbucket(key, shift);
+          const uint32_t hk = (w << 5) | sl;
+          uint32_t h = hbucket(hk, shift);
           uint4 q = tab4[h];
-          bool hit = (q.x == key) | (q.y == key) | (q.z == key) | (q.w == key);
+          bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
           while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at load <= 1/4)
             h = (h + 1) & bmask;
             q = tab4[h];
-            hit = (q.x == key) | (q.y == key) | (q.z == key) | (q.w == key);
+            hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
           }
           return hit;
         };
         // Phase 1: whole 32-word rounds of the long lists, one list at a time: all
-        // lanes read consecutive words of the same B_v, no owner lookup.
+        // lanes read consecutive words of the same list, no owner lookup.
         uint32_t longs = __ballot_sync(kFull, bl >= 32);
         while (longs) {
           const int src = __ffs(longs) - 1;
@@ -275,9 +281,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
       } else {
         const uint32_t binc = warp_incl_scan(bl, lane);
         const uint32_t total_b = __shfl_sync(kFull, binc, 31);
-        const uint32_t* A = mode == 2 ? c_ik : tab;
+        const uint32_t* A = mode == 2 ? cS : tab;
         flatten(pay, lane, bl > 0, binc - bl, make_uint4(b0, binc - bl, mode == 2 ? a0 : aoff, alen), total_b,
-                [&](uint32_t f, uint4 P) { return c_jk[P.x + (f - P.y)]; },
+                [&](uint32_t f, uint4 P) { return cP[P.x + (f - P.y)]; },
                 [&](uint32_t, uint4 P, uint32_t w) { hits += contains_sorted(A + P.z, P.w, w); });
       }
       base += L;
@@ -294,22 +300,29 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, co
 // ---- plan statistics (BBTC_PLAN_STATS): B_alg, visits, d'_max -------------------
 // Per task t and edge (u,v) of G_ij: a = d(G_ik,u), b = d(G_jk,v).
 // B_alg(t) = 4(|V_i|+1) + 8 R_ij + Σ (4 + 8 + 4a + 4b)
-__global__ void k_stats_edges(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows,
+__global__ void k_stats_edges(const uint32_t* __restrict__ it_v, const uint32_t* __restrict__ it_u,
                               const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks,
                               const TaskDesc* __restrict__ tasks, uint32_t n_exec,
                               unsigned long long* __restrict__ ab_sum) {
   for (uint32_t t = blockIdx.y; t < n_exec; t += gridDim.y) {
     const TaskDesc T = tasks[t];
     const BlockDesc Bij = blocks[T.ij], Bik = blocks[T.ik], Bjk = blocks[T.jk];
-    unsigned long long acc = 0;
+    unsigned long long sa = 0, sb = 0;
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < Bij.nnz;
          x += (uint64_t)gridDim.x * blockDim.x) {
-      const uint32_t u = rows[Bij.e0 + x], v = cols[Bij.e0 + x];
-      acc += (rowptr[Bik.ro + u + 1] - rowptr[Bik.ro + u]) + (rowptr[Bjk.ro + v + 1] - rowptr[Bjk.ro + v]);
+      const uint32_t u = it_u[Bij.e0 + x], v = it_v[Bij.e0 + x];
+      sa += rowptr[Bik.ro + u + 1] - rowptr[Bik.ro + u];
+      sb += rowptr[Bjk.ro + v + 1] - rowptr[Bjk.ro + v];
     }
 #pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&ab_sum[t], acc);
+    for (int d = 16; d >= 1; d >>= 1) {
+      sa += __shfl_xor_sync(kFull, sa, d);
+      sb += __shfl_xor_sync(kFull, sb, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (sa) atomicAdd(&ab_sum[2 * t], sa);
+      if (sb) atomicAdd(&ab_sum[2 * t + 1], sb);
+    }
   }
 }
 
@@ -354,18 +367,26 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   uint32_t max_part = 0;
   for (uint32_t i = 0; i < plan->p; ++i) max_part = std::max(max_part, plan->cuts[i + 1] - plan->cuts[i]);
   const bool hash = max_part < (1u << 27);
-  auto kern = hash ? k_count<true> : k_count<false>;
-  static int per_sm[2] = {0, 0};
-  if (!per_sm[hash]) {
+  using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
+                         const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
+                         unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t);
+  const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0);
+  static const KernT kerns[4] = {k_count<false, false>, k_count<true, false>, k_count<false, true>,
+                                 k_count<true, true>};
+  KernT kern = kerns[variant];
+  static int per_sm[4] = {0, 0, 0, 0};
+  if (!per_sm[variant]) {
     BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
-    BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[hash], kern, kWarps * 32, kSmemBytes));
+    BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[variant], kern, kWarps * 32, kSmemBytes));
   }
-  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm[hash], 1),
+  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm[variant], 1),
                                            (my_items + kWarps - 1) / kWarps);
+  const uint32_t* iu = plan->colmajor ? plan->ccu.p : plan->rows.p;
+  const uint32_t* iv = plan->colmajor ? plan->ccv.p : plan->cols.p;
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
-      plan->cols.p, plan->rows.p, plan->rowptr.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p,
-      (uint32_t)plan->tasks.size(), item_lo, item_hi, plan->chunk, rank, world, cursor,
-      (unsigned long long*)d_counts, (uint32_t)nt, ready, epoch);
+      plan->cols.p, iu, iv, plan->rowptr.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p,
+      (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
+      (uint32_t)nt, ready, epoch);
   BBTC_LAUNCHED(ctx);
 }
 
@@ -375,7 +396,7 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan) {
   const uint32_t nb = (uint32_t)plan->blocks.size();
   DevBuf<unsigned long long> ab, nonempty;
   DevBuf<uint32_t> dmax, rpb;
-  ab.alloc(ne, ctx);
+  ab.alloc(2 * ne, ctx);
   nonempty.alloc(nb, ctx);
   dmax.alloc(1, ctx);
   rpb.alloc(nb, ctx);
@@ -387,11 +408,13 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan) {
     maxrows = std::max(maxrows, h_rpb[b]);
   }
   BBTC_CUDA(cudaMemcpyAsync(rpb.p, h_rpb.data(), nb * 4, cudaMemcpyHostToDevice, st));
-  BBTC_CUDA(cudaMemsetAsync(ab.p, 0, ne * 8, st));
+  BBTC_CUDA(cudaMemsetAsync(ab.p, 0, ne * 16, st));
   BBTC_CUDA(cudaMemsetAsync(nonempty.p, 0, nb * 8, st));
   BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 4, st));
   if (ne) {
-    k_stats_edges<<<dim3(64, std::min(ne, 4096u)), 256, 0, st>>>(plan->cols.p, plan->rows.p, plan->rowptr.p,
+    k_stats_edges<<<dim3(64, std::min(ne, 4096u)), 256, 0, st>>>(plan->colmajor ? plan->ccv.p : plan->cols.p,
+                                                               plan->colmajor ? plan->ccu.p : plan->rows.p,
+                                                               plan->rowptr.p,
                                                                plan->d_blocks.p, plan->d_tasks.p, ne, ab.p);
     BBTC_LAUNCHED(ctx);
   }
@@ -400,19 +423,24 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan) {
                                                                                  rpb.p, nonempty.p, dmax.p);
     BBTC_LAUNCHED(ctx);
   }
-  std::vector<unsigned long long> h_ab(ne), h_ne(nb);
+  std::vector<unsigned long long> h_ab(2 * ne), h_ne(nb);
   uint32_t h_dmax = 0;
-  BBTC_CUDA(cudaMemcpyAsync(h_ab.data(), ab.p, ne * 8, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaMemcpyAsync(h_ab.data(), ab.p, ne * 16, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaMemcpyAsync(h_ne.data(), nonempty.p, nb * 8, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaMemcpyAsync(&h_dmax, dmax.p, 4, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaStreamSynchronize(st));
-  uint64_t balg = 0, visits = 0;
+  uint64_t balg = 0, visits = 0, suma = 0, sumb = 0;
   for (uint32_t t = 0; t < ne; ++t) {
     const TaskDesc& T = plan->tasks[t];
     const BlockDesc& Bij = plan->blocks[T.ij];
-    balg += 4ull * ((uint64_t)h_rpb[T.ij] + 1) + 8ull * h_ne[T.ij] + 12ull * Bij.nnz + 4ull * h_ab[t];
+    balg += 4ull * ((uint64_t)h_rpb[T.ij] + 1) + 8ull * h_ne[T.ij] + 12ull * Bij.nnz +
+            4ull * (h_ab[2 * t] + h_ab[2 * t + 1]);
     visits += Bij.nnz;
+    suma += h_ab[2 * t];
+    sumb += h_ab[2 * t + 1];
   }
+  plan->info.sum_a = suma;
+  plan->info.sum_b = sumb;
   plan->info.b_alg = balg;
   plan->info.visits = visits;
   plan->info.dmax_blk = h_dmax;

@@ -143,6 +143,8 @@ struct bbtc_plan {
   bbtc::DevBuf<uint32_t> cols;        // m: local column id v - cuts[j]
   bbtc::DevBuf<uint32_t> rows;        // m: local row id u - cuts[i]
   bbtc::DevBuf<uint32_t> rowptr;      // sum over blocks of |V_i|+1
+  bbtc::DevBuf<uint32_t> ccu, ccv;    // m: column-major iteration order (u, v) of each block
+  bool colmajor = true;               // kernel walks G_ij by column (ccu/ccv) vs by row (rows/cols)
   bbtc::DevBuf<BlockDesc> d_blocks;
   bbtc::DevBuf<TaskDesc> d_tasks;
   bbtc::DevBuf<uint64_t> d_item_start;
@@ -154,8 +156,21 @@ struct bbtc_plan {
   uint32_t* h_cols = nullptr;
   uint32_t* h_rows = nullptr;
   uint32_t* h_rowptr = nullptr;
+  uint32_t* h_ccu = nullptr;
+  uint32_t* h_ccv = nullptr;
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;
+
+  // The per-edge u32 arenas the count kernel reads (all indexed by edge position):
+  // cols (CSR lookups) + the iteration order arrays of the plan's mode.
+  struct EdgeArena {
+    bbtc::DevBuf<uint32_t>* dev;
+    uint32_t** host;
+  };
+  std::vector<EdgeArena> edge_arenas() {
+    if (colmajor) return {{&cols, &h_cols}, {&ccu, &h_ccu}, {&ccv, &h_ccv}};
+    return {{&cols, &h_cols}, {&rows, &h_rows}};
+  }
 };
 
 namespace bbtc {

@@ -31,15 +31,22 @@ inline unsigned grid_for(const bbtc_ctx* ctx, uint64_t n, int per_sm = 8) {
   return (unsigned)std::max<uint64_t>(1, std::min(want, cap));
 }
 
+// Runs a CUB device-wide primitive with temporary storage from the context cache.
+// `kernels` = the kernel launches the call makes (for the launch counter; matches
+// the ncu launch lists in profiles/).
 template <class F>
-void cub_call(bbtc_ctx* ctx, F f) {
+void cub_call(bbtc_ctx* ctx, F f, uint64_t kernels = 2) {
   size_t bytes = 0;
   BBTC_CUDA(f((void*)nullptr, bytes));
   DevBuf<uint8_t> tmp;
   tmp.alloc(std::max<size_t>(bytes, 1), ctx);
   BBTC_CUDA(f((void*)tmp.p, bytes));
-  ctx->launches += 1;
+  ctx->launches += kernels;
 }
+
+// Onesweep radix sort: histogram + exclusive-sum kernels, then one pass per 8-bit
+// digit for every portion of up to 2^28 items.
+inline uint64_t radix_kernels(uint64_t n, int bits) { return 2 + (uint64_t)((bits + 7) / 8) * (n / (1ull << 28) + 1); }
 
 // ---- a1 ------------------------------------------------------------------------------
 // key = (min << bw) | max for a != b, kSentinel for self-loops; tracks the largest id.
@@ -308,7 +315,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, bw + bid, st);
-    });
+    }, radix_kernels(E, bw + bid));
     tr.mark("sort1");
     DevBuf<uint64_t>& sorted = db.Current() == keys.p ? keys : alt;
     DevBuf<uint64_t>& other = db.Current() == keys.p ? alt : keys;
@@ -352,7 +359,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     const int bdeg = std::max(1, bitlen(std::min<uint64_t>(m, n - 1)));
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortPairs(t, b, deg.p, g->deg_sorted.p, ids.p, order.p, (uint64_t)n, 0, bdeg, st);
-    });
+    }, radix_kernels(n, bdeg));
     k_rank<<<grid_for(ctx, n), kThreads, 0, st>>>(order.p, n, g->rank.p);
     BBTC_LAUNCHED(ctx);
     tr.mark("rank");
@@ -451,7 +458,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     cub::DoubleBuffer<uint64_t> db(ck.p, ck_alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, db, m, 0, bp + 2 * bn, st);
-    });
+    }, radix_kernels(m, bp + 2 * bn));
     if (db.Current() != ck.p) std::swap(ck, ck_alt);
     ck_alt.reset();
     tr.mark("sort2");
@@ -508,6 +515,26 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     BBTC_LAUNCHED(ctx);
   }
   tr.mark("rowptr");
+  // Column-major iteration arrays (default): counting transpose of every block.
+  plan->colmajor = !(flags & BBTC_PLAN_ROWMAJOR);
+  if (plan->colmajor) {
+    // Per block, a stable radix sort of the (row-sorted) edges by column: keys = local
+    // column ids, values = local row ids -> CSC order with rows ascending per column.
+    plan->ccu.alloc(m, ctx);
+    plan->ccv.alloc(m, ctx);
+    for (uint32_t b = 0; b < nb; ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      if (B.nnz == 0) continue;
+      const int cb = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
+      cub_call(ctx, [&](void* t, size_t& bb) {
+        return cub::DeviceRadixSort::SortPairs(t, bb, plan->cols.p + B.e0, plan->ccv.p + B.e0, plan->rows.p + B.e0,
+                                               plan->ccu.p + B.e0, B.nnz, 0, cb, st);
+      }, radix_kernels(B.nnz, cb));
+    }
+    plan->rows.reset();   // the row-major COO is only needed to build the transpose
+    bytes += 4 * m;       // cols + ccu + ccv instead of cols + rows
+    tr.mark("transpose");
+  }
   // ---- a5: tasks and work items (host)
   plan->info.p = pe;
   plan->info.clamped = plan->clamped;

@@ -34,7 +34,7 @@ for p in ps:
         a, b, c = ev(), ev(), ev()
         a.record(stream)
         g = bb.Graph.from_edges(ctx, ds, dd, cfg.n_hint)
-        plan = bb.Plan(ctx, g, p, stats=(it == 0))
+        plan = bb.Plan(ctx, g, p, stats=(it == 0), row_major=bool(os.environ.get("ROW_MAJOR")))
         b.record(stream)
         plan.count_async(counts)
         c.record(stream)
@@ -50,4 +50,5 @@ for p in ps:
     print(json.dumps({"config": name, "p": p, "triangles": tot, "prep_ms": prep, "count_ms": cnt,
                       "step_ms": prep + cnt, "edges_per_s": info["m"] / ((prep + cnt) / 1e3),
                       "b_alg_GBps": info["b_alg"] / cnt / 1e6, "visits": info["visits"], "lambda": info["lambda"],
-                      "dmax_blk": info["dmax_blk"], "block_bytes": info["block_bytes"]}), flush=True)
+                      "dmax_blk": info["dmax_blk"], "block_bytes": info["block_bytes"],
+                      "sum_a": info["sum_a"], "sum_b": info["sum_b"]}), flush=True)

@@ -22,17 +22,17 @@ def ctx(gpu):
     return bb.Context(0)
 
 
-def run(ctx, s, d, n_hint, p=1, cuts=None, stats=False):
+def run(ctx, s, d, n_hint, p=1, cuts=None, stats=False, row_major=False):
     import paper_2009_12457_b200 as bb
     g = bb.Graph.from_edges(ctx, s, d, n_hint)
-    plan = bb.Plan(ctx, g, p, cuts, stats=stats)
+    plan = bb.Plan(ctx, g, p, cuts, stats=stats, row_major=row_major)
     tot, pt = plan.count()
     return g, plan, tot, pt
 
 
-def check(ctx, s, d, n_hint, p=1, cuts=None, og=None):
+def check(ctx, s, d, n_hint, p=1, cuts=None, og=None, row_major=False):
     og = og or oracle.OracleGraph(s, d, n_hint)
-    g, plan, tot, pt = run(ctx, s, d, n_hint, p, cuts)
+    g, plan, tot, pt = run(ctx, s, d, n_hint, p, cuts, row_major=row_major)
     ocuts = og.default_cuts(p) if cuts is None else np.asarray(cuts, np.uint32)
     assert np.array_equal(plan.cuts(), ocuts)
     otot, opt, _, _ = og.count(cuts=ocuts)
@@ -57,11 +57,12 @@ def test_karate_golden(ctx):
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_rmat16_p_grid(ctx, seed):
+@pytest.mark.parametrize("row_major", [False, True])
+def test_rmat16_p_grid(ctx, seed, row_major):
     s, d = inputs.rmat(16, 16, seed)
     og = oracle.OracleGraph(s, d, 1 << 16)
     for p in (1, 2, 3, 4, 5, 8, 16):
-        check(ctx, s, d, 1 << 16, p, og=og)
+        check(ctx, s, d, 1 << 16, p, og=og, row_major=row_major)
 
 
 def test_rmat16_preprocessing_matches_oracle(ctx):
@@ -113,14 +114,15 @@ def test_random_graphs_random_cuts(ctx, seed):
         check(ctx, s, d, n, p=p, og=og)
 
 
-def test_dense_rows_exceed_slab(ctx):
-    """K_n with long rows forces the global-memory search path (|A_u| > 1024 words)."""
+@pytest.mark.parametrize("row_major", [False, True])
+def test_dense_rows_exceed_slab(ctx, row_major):
+    """K_n with long rows forces the global-memory search path (|list| > 1024 words)."""
     n = 1400
     iu = np.triu_indices(n, 1)
     s, d = iu[0].astype(np.uint32), iu[1].astype(np.uint32)
-    g, plan, tot, pt = run(ctx, s, d, n, 1)
+    g, plan, tot, pt = run(ctx, s, d, n, 1, row_major=row_major)
     assert tot == n * (n - 1) * (n - 2) // 6
-    _, _, tot3, pt3 = run(ctx, s, d, n, cuts=[0, 300, 1400])
+    _, _, tot3, pt3 = run(ctx, s, d, n, cuts=[0, 300, 1400], row_major=row_major)
     sz = [300, 1100]
     want = [300 * 299 * 298 // 6, 300 * 299 // 2 * 1100, 300 * 1100 * 1099 // 2, 1100 * 1099 * 1098 // 6]
     assert list(pt3) == want and tot3 == tot
@@ -150,7 +152,8 @@ def test_degenerate_inputs(ctx):
         run(ctx, bad, np.array([1], np.uint32), 0, 1)
 
 
-def test_device_input_streaming_and_ranks(ctx):
+@pytest.mark.parametrize("row_major", [False, True])
+def test_device_input_streaming_and_ranks(ctx, row_major):
     """Device-resident input, host-streamed blocks (a6) and a rank split all agree."""
     import torch
     import paper_2009_12457_b200 as bb
@@ -160,7 +163,7 @@ def test_device_input_streaming_and_ranks(ctx):
     ts = torch.from_numpy(s.view(np.int32)).cuda()
     td = torch.from_numpy(d.view(np.int32)).cuda()
     g = bb.Graph.from_edges(ctx, ts, td, 1 << 15)
-    plan = bb.Plan(ctx, g, 6, stats=True)
+    plan = bb.Plan(ctx, g, 6, stats=True, row_major=row_major)
     tot, pt = plan.count()
     assert tot == otot and np.array_equal(pt, opt)
     info = plan.info()
@@ -199,15 +202,16 @@ def test_full_size_configs(ctx, name):
     check(ctx, s, d, cfg.n_hint, cfg.p, og=og)
 
 
-def test_huge_part_uses_sorted_path(ctx):
+@pytest.mark.parametrize("row_major", [False, True])
+def test_huge_part_uses_sorted_path(ctx, row_major):
     """A part with >= 2^27 vertices disables the hash keys: the sorted-slab kernel must agree."""
     s, d = inputs.rmat(14, 16, 3)
     spread = (s.astype(np.uint64) * 8209 % (1 << 27)).astype(np.uint32), \
              (d.astype(np.uint64) * 8209 % (1 << 27)).astype(np.uint32)
     n = (1 << 27) + 5
     og = oracle.OracleGraph(spread[0], spread[1], n)
-    check(ctx, spread[0], spread[1], n, p=1, og=og)
-    check(ctx, spread[0], spread[1], n, cuts=[0, (1 << 27) + 1, n], og=og)
+    check(ctx, spread[0], spread[1], n, p=1, og=og, row_major=row_major)
+    check(ctx, spread[0], spread[1], n, cuts=[0, (1 << 27) + 1, n], og=og, row_major=row_major)
 
 
 @pytest.mark.parametrize("n_hint", [0, 1, 5, 1000, 1 << 20])
