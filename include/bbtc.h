@@ -139,7 +139,8 @@ typedef struct {
  * When cuts is given, p must equal its length - 1 and is not clamped.
  * Block (i,j), i <= j, holds the edges (u,v) with u in V_i, v in V_j
  * as BCSR: row offsets uint32[|V_i|+1] over local row ids u - cuts[i], column ids
- * uint32 v - cuts[j] (rows ascending), plus the local row id of every edge.
+ * uint32 v - cuts[j] (rows ascending; the columns inside a row are in no particular
+ * order), plus the local row id of every edge.
  * Errors: BBTC_EINVAL (p == 0, bad cuts), BBTC_ERANGE (2*ceil(log2 n) +
  * ceil(log2 p) > 64 bits of sort key), BBTC_ENOMEM, BBTC_ECUDA. */
 BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,

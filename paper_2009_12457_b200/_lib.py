@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbbtc.so")
+# BBTC_LIB overrides the library path (A/B builds of the same ABI); the default is in-tree.
+LIB_PATH = os.environ.get("BBTC_LIB") or os.path.join(_HERE, "libbbtc.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "

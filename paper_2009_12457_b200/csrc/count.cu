@@ -3,21 +3,16 @@
 // Alg. 5 BB-TC-LIST: for task t = (i,j,k) and every edge (u,v) of
 // G_ij, count |N(G_ik,u) ∩ N(G_jk,v)|, summed into the task's uint64 counter.
 //
-// B200 design: one persistent grid, one warp per work item
-// (task t, a range of `chunk` consecutive edges of G_ij), items claimed from a
-// global atomic cursor.  A warp takes 32 edges at a time, and
-//   1. stages every distinct row list A_u = N(G_ik,u) of those edges into its
-//      shared-memory slab (the edges are row-sorted, so rows repeat across lanes
-//      and each A_u is read from HBM once per batch, not once per edge);
-//   2. flattens the 32 probe lists B_v = N(G_jk,v) into one virtual array and
-//      walks it 32 elements per step — consecutive lanes read consecutive words of
-//      the same list (coalesced), no lane idles on short lists;
-//   3. looks each probe w up in its edge's staged A_u by binary search in shared
-//      memory: w ∈ A_u  <=>  w is a common neighbour, i.e. one triangle.
-// This computes exactly Σ_(u,v) |A_u ∩ B_v| (what Alg. 1's merge returns), with
-// every lane busy whatever the list-length skew.  Rows whose A_u exceeds the
-// slab are searched in global memory instead (rare: d'_max is small after the
-// degree ordering).
+// B200 design: one persistent grid, one warp per work item (task t,
+// a range of consecutive edges of G_ij sized to equal estimated work), items
+// claimed from a global atomic cursor.  A warp takes 32 consecutive edges of G_ij
+// in its walk order (column order by default), so one of the two lists of an edge
+// repeats across neighbouring lanes: that "staged" list S (N(G_jk,v) by column,
+// N(G_ik,u) by row) is inserted once into a per-warp shared-memory hash table, and
+// every word w of the other, "probe" list P is looked up in it: w ∈ S  <=>  w is a
+// common neighbour, i.e. one triangle.  This computes exactly Σ_(u,v) |S ∩ P|,
+// what Alg. 1's merge returns per edge, with every lane busy whatever the skew of
+// the list lengths, and needs no order inside the lists.
 #include <cub/cub.cuh>
 
 #include "internal.h"
@@ -26,11 +21,15 @@ namespace bbtc {
 namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
-constexpr int kTable = 1024;         // per-warp shared words: hash table or sorted slab (4 KiB)
-constexpr int kHashCap = kTable / 4; // staged A words per batch in hash mode (load <= 1/4)
+constexpr int kTable = 1024;         // per-warp shared words: one hash table of 4-word buckets (4 KiB)
+constexpr int kHashCap = kTable / 4; // staged words of a shared (multi-list) table (load <= 1/4)
+constexpr int kChunk = kTable / 2;   // staged words of a single-list table fill (load <= 1/2)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr size_t kSmemBytes = (size_t)kWarps * (kTable * 4 + 32 * 16);
+constexpr int kCtasPerSm = 8;        // cap on resident CTAs per SM (BBTC_CTAS_PER_SM overrides)
+constexpr int kMinCtas = 5;          // register budget: >= 5 CTAs (40 warps) resident per SM
+constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 #pragma unroll
@@ -44,25 +43,14 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 __device__ __forceinline__ uint32_t lanemask_le(int lane) { return 0xffffffffu >> (31 - lane); }
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-// lower_bound search of w in the sorted list A[0..len): true if present.
-__device__ __forceinline__ bool contains_sorted(const uint32_t* A, uint32_t len, uint32_t w) {
-  uint32_t lo = 0, n = len;
-  while (n > 0) {
-    uint32_t half = n >> 1;
-    if (A[lo + half] < w) { lo += half + 1; n -= half + 1; }
-    else n = half;
-  }
-  return lo < len && A[lo] == w;
-}
-
 __device__ __forceinline__ uint32_t hbucket(uint32_t key, int shift) { return (key * 0x9E3779B1u) >> shift; }
 
 // Segmented flatten: the warp walks the concatenation of per-lane segments
 // [start, start+len) (start = exclusive prefix of len over lanes) 32 positions at a
 // time.  Non-empty segments are compacted into `pay` (one uint4 payload each); the
 // owner of each position is found with one redux.or of the segment starts falling in
-// the current window plus a popc.  `load(f, P)` fetches the position's word one
-// window ahead of `use(f, P, w)` (software pipelining of the gather).
+// the current window plus a popc.  `load(f, P)` fetches the position's word two
+// windows ahead of `use(f, P, w)` (software pipelining of the gather).
 template <class Ld, class Use>
 __device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uint32_t start, uint4 payload,
                                         uint32_t total, Ld load, Use use) {
@@ -78,8 +66,6 @@ __device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uin
     before += __popc(starts);
     return idx;
   };
-  // Two windows in flight: the gathers of windows f0+32 and f0+64 overlap the
-  // probes of window f0.
   uint4 P0 = pay[owner(0)], P1 = P0;
   uint32_t w0 = lane < total ? load(lane, P0) : 0, w1 = 0;
   if (32 < total) {
@@ -101,16 +87,96 @@ __device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uin
   __syncwarp();
 }
 
-// Alg. 5 over work items.  Each edge (u,v) of G_ij needs |N(G_ik,u) ∩ N(G_jk,v)|.
-// The edges of a batch are consecutive in the block's iteration order, so one of
-// the two lists repeats across neighbouring lanes: the "staged" list S (N(G_jk,v)
-// when walking by column, kCol; N(G_ik,u) when walking by row) is put in shared
-// memory once per distinct key, and every word of the other, "probe" list P is
-// looked up in it.  kHash: staged lists share one hash table of 4-word buckets
-// keyed by (w << 5 | slot) (needs |V_k| < 2^27); otherwise (and for lists too long
-// for the table) they are staged sorted and searched by binary search.
-template <bool kHash, bool kCol>
-__global__ void __launch_bounds__(kWarps * 32)
+// Inserts key hk into the table of 4-word buckets (linear probing over buckets).
+__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t hk, int shift, uint32_t bmask) {
+  uint32_t h = hbucket(hk, shift);
+  for (;;) {
+    uint32_t* bk = tab + 4 * h;
+    if (atomicCAS(bk + 0, kEmpty, hk) == kEmpty) return;
+    if (atomicCAS(bk + 1, kEmpty, hk) == kEmpty) return;
+    if (atomicCAS(bk + 2, kEmpty, hk) == kEmpty) return;
+    if (atomicCAS(bk + 3, kEmpty, hk) == kEmpty) return;
+    h = (h + 1) & bmask;
+  }
+}
+
+__device__ __forceinline__ uint32_t table_probe(const uint4* tab4, uint32_t hk, int shift, uint32_t bmask) {
+  uint32_t h = hbucket(hk, shift);
+  uint4 q = tab4[h];
+  bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
+  while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at these loads)
+    h = (h + 1) & bmask;
+    q = tab4[h];
+    hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
+  }
+  return hit;
+}
+
+// Probe lists of lanes: P = cols[bx .. bx + bl).  Phase 1 walks the long lists one at
+// a time in whole 32-word rounds (all lanes on consecutive words of one list, four
+// loads in flight); phase 2 flattens the < 32-word remainders across the lanes.
+// key(w, slot) gives the table key of a probe word.
+template <class Key>
+__device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ cols, const uint4* tab4, uint4* pay,
+                                                int lane, uint32_t bx, uint32_t bl, uint32_t slot, int shift,
+                                                uint32_t bmask, Key key) {
+  uint32_t hits = 0;
+  uint32_t longs = __ballot_sync(kFull, bl >= 32);
+  while (longs) {
+    const int src = __ffs(longs) - 1;
+    longs &= longs - 1;
+    const uint32_t* B = cols + __shfl_sync(kFull, bx, src) + lane;
+    const uint32_t nfull = __shfl_sync(kFull, bl, src) & ~31u;
+    const uint32_t sl = __shfl_sync(kFull, slot, src);
+    uint32_t off = 0;
+    for (; off + 128 <= nfull; off += 128) {
+      const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
+      hits += table_probe(tab4, key(w1, sl), shift, bmask) + table_probe(tab4, key(w2, sl), shift, bmask) +
+              table_probe(tab4, key(w3, sl), shift, bmask) + table_probe(tab4, key(w4, sl), shift, bmask);
+    }
+    for (; off < nfull; off += 32) hits += table_probe(tab4, key(B[off], sl), shift, bmask);
+  }
+  const uint32_t rem = bl & 31u;
+  const uint32_t rinc = warp_incl_scan(rem, lane);
+  const uint32_t total_r = __shfl_sync(kFull, rinc, 31);
+  const uint32_t rstart = rinc - rem;
+  flatten(pay, lane, rem > 0, rstart, make_uint4(bx + (bl & ~31u) - rstart, slot, 0, 0), total_r,
+          [&](uint32_t f, uint4 P) { return cols[P.x + f]; },
+          [&](uint32_t, uint4 P, uint32_t w) { hits += table_probe(tab4, key(w, P.y), shift, bmask); });
+  return hits;
+}
+
+// The rare path, kept out of line so it does not weigh on the main loop's code: one
+// staged list S = cS[s0 .. s0+total_a) longer than a shared table (or any list
+// when slot tags do not fit in 32 bits), hashed alone with untagged keys in chunks
+// of kChunk words.  |S ∩ P| is additive over a partition of S, so every probe list
+// is probed once per chunk.  Returns this lane's hits.
+__device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ cS,
+                                           uint32_t s0, uint32_t total_a, uint32_t bx, uint32_t bl, uint32_t* tab,
+                                           uint4* pay, int lane) {
+  uint4* tab4 = reinterpret_cast<uint4*>(tab);
+  uint32_t hits = 0;
+  for (uint32_t c0 = 0; c0 < total_a; c0 += kChunk) {
+    const uint32_t cn = min((uint32_t)kChunk, total_a - c0);
+    uint32_t nb = 16;
+    while (2 * nb < cn) nb <<= 1;
+    const uint32_t bmask = nb - 1;
+    const int shift = 32 - (__ffs(nb) - 1);
+    for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    __syncwarp();
+    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, cS[s0 + c0 + x], shift, bmask);
+    __syncwarp();
+    hits += probe_lists(cols, tab4, pay, lane, bx, bl, 0, shift, bmask, [](uint32_t w, uint32_t) { return w; });
+  }
+  return hits;
+}
+
+// Alg. 5 over work items.  kSlots: batches of several staged lists share one table
+// with slot-tagged keys (w << 5 | slot), which needs |V_k| < 2^27; otherwise every
+// batch takes one staged list at a time (long_list).  kCol: walk G_ij by column
+// (ccu/ccv arrays, stage N(G_jk,v)) or by row (rows/cols, stage N(G_ik,u)).
+template <bool kSlots, bool kCol>
+__global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
         const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
@@ -122,7 +188,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
   uint32_t* tab = smem + wid * kTable;
   uint4* tab4 = reinterpret_cast<uint4*>(tab);
   uint4* pay = reinterpret_cast<uint4*>(smem + kWarps * kTable) + wid * 32;
-  constexpr uint32_t kCap = kHash ? kHashCap : kTable;
 
   for (;;) {
     unsigned long long it = 0;
@@ -140,11 +205,12 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     if (ready) {
       // Streaming (a6): wait until the copy engine has delivered the task's blocks.
       if (lane == 0) {
-        for (uint32_t b : {T.ij, T.ik, T.jk}) {
+        const uint32_t need[3] = {T.ij, T.ik, T.jk};
+        for (int x = 0; x < 3; ++x) {
           uint32_t rv;
           uint64_t spins = 0;
           do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(rv) : "l"(ready + b) : "memory");
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(rv) : "l"(ready + need[x]) : "memory");
             if (rv != epoch) {
               __nanosleep(1000);
               if (++spins > (1ull << 25)) __trap();   // ~30 s without the copy: fail, never hang
@@ -162,7 +228,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     const uint32_t* rpS = rowptr + BS.ro;
     const uint32_t* cS = cols + BS.e0;
     const uint32_t* rpP = rowptr + BP.ro;
-    const uint32_t* cP = cols + BP.e0;
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
@@ -191,100 +256,41 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const uint32_t incl = warp_incl_scan(lead_len, lane);
       const uint32_t aoff = __shfl_sync(kFull, incl - lead_len, my_leader);
       const uint32_t aend = aoff + alen;
-      int L = __popc(__ballot_sync(kFull, valid && aend <= kCap));   // lanes [0,L) fit
-      // mode: 0 = hash (or sorted slab in the !kHash kernel), 1 = sorted slab, 2 = global
-      int mode = 0;
-      bool dense = false;   // single long list hashed at load <= 1/2
+      // lanes [0,L) whose staged lists fit one shared table (load <= 1/4)
+      int L = kSlots ? __popc(__ballot_sync(kFull, valid && aend <= kHashCap)) : 0;
+      bool dense = false;   // one list of kHashCap..kChunk words: a table of its own, load <= 1/2
+      bool longl = false;   // longer (or untaggable): the out-of-line chunked path
       if (L == 0) {
-        // The first staged list alone exceeds the table: take its edges alone.
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         const uint32_t a_first = __shfl_sync(kFull, alen, 0);
         L = __popc(__ballot_sync(kFull, valid && key == k0));
-        if (kHash && a_first <= 2 * kHashCap) dense = true;
-        else mode = a_first <= kTable ? 1 : 2;
-      } else if (!kHash) {
-        mode = 1;
+        if (kSlots && a_first <= kChunk) dense = true;
+        else longl = true;
       }
       const bool in = lane < L;
-      int shift = 0;
-      uint32_t bmask = 0;
-      if (mode < 2) {
-        // ---- stage the distinct lists S of lanes [0,L)
-        const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
-        if (kHash && mode == 0) {
+      // edges whose staged list is empty cannot close a triangle: no probes for them
+      const uint32_t bl = (in && alen > 0) ? blen : 0;
+      const uint32_t bx = (uint32_t)BP.e0 + b0;   // index of P[0] in the cols arena
+      if (__any_sync(kFull, bl > 0)) {
+        if (longl) {
+          hits += long_list(cols, cS, __shfl_sync(kFull, a0, 0), __shfl_sync(kFull, alen, 0), bx, bl, tab, pay,
+                            lane);
+        } else {
+          // ---- stage the distinct lists S of lanes [0,L) into one table
+          const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
           uint32_t nb = 16;
           while ((dense ? 2 * nb : nb) < total_a) nb <<= 1;
-          bmask = nb - 1;
-          shift = 32 - (__ffs(nb) - 1);
+          const uint32_t bmask = nb - 1;
+          const int shift = 32 - (__ffs(nb) - 1);
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, slot, 0), total_a,
                   [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
-                  [&](uint32_t, uint4 P, uint32_t w) {
-                    const uint32_t hk = (w << 5) | P.z;
-                    uint32_t h = hbucket(hk, shift);
-                    for (;;) {
-                      uint32_t* bk = tab + 4 * h;
-                      if (atomicCAS(bk + 0, kEmpty, hk) == kEmpty) break;
-                      if (atomicCAS(bk + 1, kEmpty, hk) == kEmpty) break;
-                      if (atomicCAS(bk + 2, kEmpty, hk) == kEmpty) break;
-                      if (atomicCAS(bk + 3, kEmpty, hk) == kEmpty) break;
-                      h = (h + 1) & bmask;
-                    }
-                  });
-        } else {
-          flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, 0, 0), total_a,
-                  [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
-                  [&](uint32_t f, uint4, uint32_t w) { tab[f] = w; });
+                  [&](uint32_t, uint4 P, uint32_t w) { table_insert(tab, (w << 5) | P.z, shift, bmask); });
+          // ---- probe every word of each lane's list P against its staged list
+          hits += probe_lists(cols, tab4, pay, lane, bx, bl, slot, shift, bmask,
+                              [](uint32_t w, uint32_t sl) { return (w << 5) | sl; });
         }
-      }
-      // ---- probe every word w of each lane's list P against its staged list
-      const uint32_t bl = in ? blen : 0;
-      if (kHash && mode == 0) {
-        const uint32_t bx = (uint32_t)BP.e0 + b0;   // index of P[0] in the cols arena
-        auto probe = [&](uint32_t w, uint32_t sl) -> uint32_t {
-          const uint32_t hk = (w << 5) | sl;
-          uint32_t h = hbucket(hk, shift);
-          uint4 q = tab4[h];
-          bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
-          while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at load <= 1/4)
-            h = (h + 1) & bmask;
-            q = tab4[h];
-            hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
-          }
-          return hit;
-        };
-        // Phase 1: whole 32-word rounds of the long lists, one list at a time: all
-        // lanes read consecutive words of the same list, no owner lookup.
-        uint32_t longs = __ballot_sync(kFull, bl >= 32);
-        while (longs) {
-          const int src = __ffs(longs) - 1;
-          longs &= longs - 1;
-          const uint32_t* B = cols + __shfl_sync(kFull, bx, src) + lane;
-          const uint32_t nfull = __shfl_sync(kFull, bl, src) & ~31u;
-          const uint32_t sl = __shfl_sync(kFull, slot, src);
-          uint32_t off = 0;
-          for (; off + 128 <= nfull; off += 128) {
-            const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
-            hits += probe(w1, sl) + probe(w2, sl) + probe(w3, sl) + probe(w4, sl);
-          }
-          for (; off < nfull; off += 32) hits += probe(B[off], sl);
-        }
-        // Phase 2: the remainders (< 32 words per list) flattened across the lanes.
-        const uint32_t rem = bl & 31u;
-        const uint32_t rinc = warp_incl_scan(rem, lane);
-        const uint32_t total_r = __shfl_sync(kFull, rinc, 31);
-        const uint32_t rstart = rinc - rem;
-        flatten(pay, lane, rem > 0, rstart, make_uint4(bx + (bl & ~31u) - rstart, slot, 0, 0), total_r,
-                [&](uint32_t f, uint4 P) { return cols[P.x + f]; },
-                [&](uint32_t, uint4 P, uint32_t w) { hits += probe(w, P.y); });
-      } else {
-        const uint32_t binc = warp_incl_scan(bl, lane);
-        const uint32_t total_b = __shfl_sync(kFull, binc, 31);
-        const uint32_t* A = mode == 2 ? cS : tab;
-        flatten(pay, lane, bl > 0, binc - bl, make_uint4(b0, binc - bl, mode == 2 ? a0 : aoff, alen), total_b,
-                [&](uint32_t f, uint4 P) { return cP[P.x + (f - P.y)]; },
-                [&](uint32_t, uint4 P, uint32_t w) { hits += contains_sorted(A + P.z, P.w, w); });
       }
       base += L;
     }
@@ -377,10 +383,21 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   static int per_sm[4] = {0, 0, 0, 0};
   if (!per_sm[variant]) {
     BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+    // Shared-memory carveout: what the resident CTAs need, the rest stays L1 for the
+    // gathered lists (BBTC_CARVEOUT = percent overrides).
+    const char* ce = getenv("BBTC_CARVEOUT");
+    const int carve = ce ? atoi(ce) : kCarveoutPct;
+    if (carve > 0) BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[variant], kern, kWarps * 32, kSmemBytes));
   }
-  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * std::max(per_sm[variant], 1),
-                                           (my_items + kWarps - 1) / kWarps);
+  // Resident CTAs per SM: the occupancy limit, capped by kCtasPerSm (more warps
+  // in flight than this only widen the working set the L2 has to hold).
+  static const int cap_env = [] {
+    const char* e = getenv("BBTC_CTAS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  const int per = std::max(1, std::min(per_sm[variant], cap_env > 0 ? cap_env : kCtasPerSm));
+  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
   const uint32_t* iu = plan->colmajor ? plan->ccu.p : plan->rows.p;
   const uint32_t* iv = plan->colmajor ? plan->ccv.p : plan->cols.p;
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(

@@ -154,9 +154,10 @@ __device__ __forceinline__ uint32_t part_of(const uint32_t* cuts, uint32_t p, ui
   return lo;
 }
 
-// Block sort key: (j, ru, rw) with j = part(rw).  Sorting by it lays the blocks out
-// contiguously in column-major block order, rows ascending inside a block and the
-// columns of each row ascending (what Alg. 1 needs: "A and B are sorted").
+// Block sort key: (j, ru, rw) with j = part(rw).  Sorting by its (j, ru) bits lays the
+// blocks out contiguously in column-major block order with rows ascending inside a
+// block; the columns of a row keep no order (the count kernel hashes the lists, so
+// Alg. 1's "A and B are sorted" is not needed).
 __global__ void k_block_keys(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
                              uint32_t p, int bn, uint64_t* __restrict__ ckeys) {
   extern __shared__ uint32_t s_cuts[];
@@ -236,6 +237,31 @@ __global__ void k_row_local(const BlockDesc* __restrict__ blocks, const uint32_t
   const uint32_t base = (uint32_t)B.e0;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < len; r += gridDim.x * blockDim.x)
     rowptr[B.ro + r] -= base;
+}
+
+// Transpose keys: (block of edge e) << cb | local column.  Blocks are contiguous edge
+// ranges, found by binary search over their first edges (held in shared memory).
+template <class K>
+__global__ void k_transpose_keys(const uint32_t* __restrict__ cols, uint64_t m, const BlockDesc* __restrict__ blocks,
+                                 uint32_t nb, int cb, K* __restrict__ keys) {
+  extern __shared__ uint64_t s_e0[];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) s_e0[b] = blocks[b].e0;
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nb - 1;   // last block with e0 <= e
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (s_e0[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    keys[e] = ((K)lo << cb) | cols[e];
+  }
+}
+
+template <class K>
+__global__ void k_low_bits(const K* __restrict__ keys, uint64_t m, int cb, uint32_t* __restrict__ out) {
+  const K mask = ((K)1 << cb) - 1;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+    out[e] = (uint32_t)(keys[e] & mask);
 }
 
 }  // namespace
@@ -457,8 +483,10 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     ck_alt.alloc(m, ctx);
     cub::DoubleBuffer<uint64_t> db(ck.p, ck_alt.p);
     cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, db, m, 0, bp + 2 * bn, st);
-    }, radix_kernels(m, bp + 2 * bn));
+      // Only the (j, ru) bits: the count kernel hashes lists, so the columns of a row
+      // need no order (sorting them too would cost 3 more radix passes).
+      return cub::DeviceRadixSort::SortKeys(t, b, db, m, getenv("BBTC_SORT_ROWS") ? 0 : bn, bp + 2 * bn, st);
+    }, radix_kernels(m, bp + bn));
     if (db.Current() != ck.p) std::swap(ck, ck_alt);
     ck_alt.reset();
     tr.mark("sort2");
@@ -515,21 +543,41 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     BBTC_LAUNCHED(ctx);
   }
   tr.mark("rowptr");
-  // Column-major iteration arrays (default): counting transpose of every block.
+  // Column-major iteration arrays (default): transpose of every block.
   plan->colmajor = !(flags & BBTC_PLAN_ROWMAJOR);
   if (plan->colmajor) {
-    // Per block, a stable radix sort of the (row-sorted) edges by column: keys = local
-    // column ids, values = local row ids -> CSC order with rows ascending per column.
+    // One stable radix sort of all edges by (block, local column): values = local
+    // row ids -> every block in CSC order, rows ascending per column, blocks in place.
     plan->ccu.alloc(m, ctx);
     plan->ccv.alloc(m, ctx);
-    for (uint32_t b = 0; b < nb; ++b) {
-      const BlockDesc& B = plan->blocks[b];
-      if (B.nnz == 0) continue;
-      const int cb = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
+    uint32_t maxw = 1;
+    for (uint32_t j = 0; j < pe; ++j) maxw = std::max(maxw, plan->cuts[j + 1] - plan->cuts[j]);
+    const int cb = std::max(1, bitlen(maxw - 1));
+    const int kb = bitlen(nb - 1);
+    if (m && kb + cb <= 32) {
+      DevBuf<uint32_t> keys;
+      keys.alloc(m, ctx);
+      k_transpose_keys<uint32_t><<<grid_for(ctx, m), kThreads, (size_t)nb * 8, st>>>(
+          plan->cols.p, m, plan->d_blocks.p, nb, cb, keys.p);
+      BBTC_LAUNCHED(ctx);
       cub_call(ctx, [&](void* t, size_t& bb) {
-        return cub::DeviceRadixSort::SortPairs(t, bb, plan->cols.p + B.e0, plan->ccv.p + B.e0, plan->rows.p + B.e0,
-                                               plan->ccu.p + B.e0, B.nnz, 0, cb, st);
-      }, radix_kernels(B.nnz, cb));
+        return cub::DeviceRadixSort::SortPairs(t, bb, keys.p, plan->ccv.p, plan->rows.p, plan->ccu.p, m, 0, kb + cb,
+                                               st);
+      }, radix_kernels(m, kb + cb));
+      k_low_bits<uint32_t><<<grid_for(ctx, m), kThreads, 0, st>>>(plan->ccv.p, m, cb, plan->ccv.p);
+      BBTC_LAUNCHED(ctx);
+    } else if (m) {
+      DevBuf<uint64_t> keys, sorted;
+      keys.alloc(m, ctx);
+      sorted.alloc(m, ctx);
+      k_transpose_keys<uint64_t><<<grid_for(ctx, m), kThreads, (size_t)nb * 8, st>>>(
+          plan->cols.p, m, plan->d_blocks.p, nb, cb, keys.p);
+      BBTC_LAUNCHED(ctx);
+      cub_call(ctx, [&](void* t, size_t& bb) {
+        return cub::DeviceRadixSort::SortPairs(t, bb, keys.p, sorted.p, plan->rows.p, plan->ccu.p, m, 0, kb + cb, st);
+      }, radix_kernels(m, kb + cb));
+      k_low_bits<uint64_t><<<grid_for(ctx, m), kThreads, 0, st>>>(sorted.p, m, cb, plan->ccv.p);
+      BBTC_LAUNCHED(ctx);
     }
     plan->rows.reset();   // the row-major COO is only needed to build the transpose
     bytes += 4 * m;       // cols + ccu + ccv instead of cols + rows
