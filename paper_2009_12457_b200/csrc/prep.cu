@@ -554,7 +554,18 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     for (uint32_t j = 0; j < pe; ++j) maxw = std::max(maxw, plan->cuts[j + 1] - plan->cuts[j]);
     const int cb = std::max(1, bitlen(maxw - 1));
     const int kb = bitlen(nb - 1);
-    if (m && kb + cb <= 32) {
+    if (m && nb <= 36) {
+      // Few blocks: sort each block in place by its local column (no key pass).
+      for (uint32_t b = 0; b < nb; ++b) {
+        const BlockDesc& B = plan->blocks[b];
+        if (B.nnz == 0) continue;
+        const int bits = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
+        cub_call(ctx, [&](void* t, size_t& bb) {
+          return cub::DeviceRadixSort::SortPairs(t, bb, plan->cols.p + B.e0, plan->ccv.p + B.e0, plan->rows.p + B.e0,
+                                                 plan->ccu.p + B.e0, B.nnz, 0, bits, st);
+        }, radix_kernels(B.nnz, bits));
+      }
+    } else if (m && kb + cb <= 32) {
       DevBuf<uint32_t> keys;
       keys.alloc(m, ctx);
       k_transpose_keys<uint32_t><<<grid_for(ctx, m), kThreads, (size_t)nb * 8, st>>>(
