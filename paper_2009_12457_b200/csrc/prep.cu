@@ -65,6 +65,45 @@ __global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __rest
   if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
 }
 
+// Hash-set canonicalisation: every raw pair's key (min << bw | max) is inserted into
+// an open-addressing table of 2^k u64 slots (load <= 1/2, linear probing); the
+// table then holds each undirected edge once (duplicates and both orientations
+// collapse to one key, self-loops are dropped).  One pass of random 8-byte CAS
+// instead of a full radix sort + unique.
+__global__ void k_canon_insert(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t E, int bw,
+                               unsigned long long* __restrict__ table, int tbits, uint32_t* __restrict__ max_id) {
+  uint32_t mx = 0;
+  const uint64_t tmask = (1ull << tbits) - 1;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = src[e], b = dst[e];
+    const uint32_t lo = min(a, b), hi = max(a, b);
+    mx = max(mx, hi);
+    if (a == b) continue;
+    const unsigned long long key = ((unsigned long long)lo << bw) | hi;
+    uint64_t h = (key * 0x9E3779B97F4A7C15ull) >> (64 - tbits);
+    for (;;) {
+      const unsigned long long old = atomicCAS(&table[h], kSentinel, key);
+      if (old == kSentinel || old == key) break;
+      h = (h + 1) & tmask;
+    }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
+}
+
+struct NotEmpty {
+  __host__ __device__ bool operator()(uint64_t k) const { return k != kSentinel; }
+};
+
+// Degrees of a list of unique keys in no particular order.
+__global__ void k_degree_any(const uint64_t* __restrict__ keys, uint64_t m, int bw, uint32_t* __restrict__ deg) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    atomicAdd(&deg[(uint32_t)(k >> bw)], 1u);
+    atomicAdd(&deg[(uint32_t)(k & ((1ull << bw) - 1))], 1u);
+  }
+}
+
 // ---- a2 ------------------------------------------------------------------------------
 __global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, int bw, uint32_t* __restrict__ deg) {
   // Warp-uniform trip count so the whole warp stays converged for __match_any_sync.
@@ -275,15 +314,38 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   DevBuf<uint32_t> dmax;
   dmax.alloc(2, ctx);
   BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
-  DevBuf<uint64_t> keys;
-  keys.alloc(E, ctx);
+  // Canonicalisation strategy: radix sort + unique (default) or a hash set
+  // (BBTC_DEDUP=hash); both yield the same edge set.  The hash set skips the sort
+  // but was measured slower end to end on B200 (friendster: 187 ms of random CAS vs
+  // 131 ms of sort, and the unsorted keys then cost 2x in the degree and orient
+  // passes, which read the sorted keys' neighbours from cache), so sort is default.
+  static const bool use_hash = [] {
+    const char* e = getenv("BBTC_DEDUP");
+    return e && std::string(e) == "hash";
+  }();
+  DevBuf<uint64_t> keys;                 // sort: one key per raw pair
+  DevBuf<unsigned long long> table;      // hash: the open-addressing set
+  int tbits = 0;
+  if (use_hash) {
+    tbits = std::max(10, bitlen(std::max<uint64_t>(E, 1) * 2 - 1));
+    table.alloc(1ull << tbits, ctx);
+  } else {
+    keys.alloc(E, ctx);
+  }
   int bw = n_hint > 1 ? std::max(1, bitlen(n_hint - 1)) : 32;
+  auto launch_canon = [&](const uint32_t* s, const uint32_t* d, uint64_t len, uint64_t c0, int width) {
+    if (use_hash)
+      k_canon_insert<<<grid_for(ctx, len), kThreads, 0, st>>>(s, d, len, width, table.p, tbits, dmax.p);
+    else
+      k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(s, d, len, width, keys.p + c0, dmax.p);
+    BBTC_LAUNCHED(ctx);
+  };
   auto canon = [&](int width) {
     BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
+    if (use_hash) BBTC_CUDA(cudaMemsetAsync(table.p, 0xFF, (1ull << tbits) * 8, st));
     if (!E) return;
     if (mem == BBTC_MEM_DEVICE) {
-      k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, width, keys.p, dmax.p);
-      BBTC_LAUNCHED(ctx);
+      launch_canon(src, dst, E, 0, width);
       return;
     }
     // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
@@ -306,9 +368,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
       BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
       BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
-      k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(ds.p + slot * chunk, dd.p + slot * chunk, len, width,
-                                                        keys.p + c0, dmax.p);
-      BBTC_LAUNCHED(ctx);
+      launch_canon(ds.p + slot * chunk, dd.p + slot * chunk, len, c0, width);
       BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
     }
     for (int x = 0; x < 2; ++x) {
@@ -335,7 +395,20 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   // Sort the canonical keys over their live bits (hi id in [0,bid), lo id in [bw,bw+bid)).
   uint64_t m = 0;
   DevBuf<uint64_t> ukeys;
-  if (E) {
+  if (E && use_hash) {
+    // The set's occupied slots are the unique edges (in no particular order).
+    const uint64_t T = 1ull << tbits;
+    ukeys.alloc(E, ctx);
+    DevBuf<uint64_t> nsel;
+    nsel.alloc(1, ctx);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::If(t, b, (const uint64_t*)table.p, ukeys.p, nsel.p, T, NotEmpty{}, st);
+    });
+    BBTC_CUDA(cudaMemcpyAsync(&m, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    table.reset();
+    tr.mark("compact");
+  } else if (E) {
     DevBuf<uint64_t> alt;
     alt.alloc(E, ctx);
     cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
@@ -372,7 +445,10 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   g->okeys.alloc(m, ctx);
   if (n) {
     BBTC_CUDA(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
-    if (m) {
+    if (m && use_hash) {
+      k_degree_any<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
+      BBTC_LAUNCHED(ctx);
+    } else if (m) {
       k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
       BBTC_LAUNCHED(ctx);
     }
