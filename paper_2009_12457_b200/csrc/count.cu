@@ -288,8 +288,29 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                   [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
                   [&](uint32_t, uint4 P, uint32_t w) { table_insert(tab, (w << 5) | P.z, shift, bmask); });
           // ---- probe every word of each lane's list P against its staged list
-          hits += probe_lists(cols, tab4, pay, lane, bx, bl, slot, shift, bmask,
-                              [](uint32_t w, uint32_t sl) { return (w << 5) | sl; });
+          auto tagged = [](uint32_t w, uint32_t sl) { return (w << 5) | sl; };
+          hits += probe_lists(cols, tab4, pay, lane, bx, bl, slot, shift, bmask, tagged);
+          // ---- a staged list that fills the whole batch usually continues (a column
+          // with many edges): keep its table and probe the run's next edges against
+          // it, instead of re-reading and re-hashing the list for every 32 edges.
+          const uint32_t k0 = __shfl_sync(kFull, key, 0);
+          if (L == 32 && __all_sync(kFull, valid && key == k0)) {
+            for (;;) {
+              const uint64_t e2 = base + L + lane;
+              const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
+              const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
+              if (L2 == 0) break;
+              uint32_t b2 = 0, bl2 = 0;
+              if (ok && alen > 0) {
+                const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
+                b2 = rpP[p2];
+                bl2 = rpP[p2 + 1] - b2;
+              }
+              hits += probe_lists(cols, tab4, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, shift, bmask, tagged);
+              L += L2;
+              if (L2 < 32) break;
+            }
+          }
         }
       }
       base += L;
