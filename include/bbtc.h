@@ -155,6 +155,13 @@ BBTC_API bbtc_status bbtc_plan_block(bbtc_ctx* ctx, const bbtc_plan* plan, uint3
 /* a6: moves the blocks into pinned host memory and releases their device copy
  * (the out-of-core form of the plan).  bbtc_count then streams them. */
 BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan);
+/* Out-of-core mode ("three subgraphs can fit into memory of the computing
+ * devices"): a host-resident plan counted by bbtc_count keeps at most `bytes` of
+ * blocks on the device.  Tasks are processed in execution order in windows whose
+ * blocks fit; blocks still needed stay resident, others are evicted, missing ones
+ * are streamed in.  0 = no limit (every block copied once).  Errors: BBTC_EINVAL;
+ * bbtc_count fails with BBTC_ERANGE if one task's three blocks exceed the budget. */
+BBTC_API bbtc_status bbtc_plan_set_budget(bbtc_plan* plan, uint64_t bytes);
 BBTC_API void bbtc_plan_free(bbtc_plan* plan);
 
 /* Task numbering (Alg. 4): tasks i <= j <= k in loop order.

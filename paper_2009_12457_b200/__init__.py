@@ -187,6 +187,10 @@ class Plan:
     def to_host(self):
         L.check(L.bbtc_plan_to_host(self.ctx.handle, self._h))
 
+    def set_budget(self, nbytes: int):
+        """Out-of-core: keep at most nbytes of blocks on the device when counting a host plan."""
+        L.check(L.bbtc_plan_set_budget(self._h, nbytes))
+
     def stage(self):
         L.check(L.bbtc_stage(self.ctx.handle, self._h))
 

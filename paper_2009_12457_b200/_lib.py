@@ -82,6 +82,7 @@ bbtc_plan_info_get = _sig("bbtc_plan_info_get", _st, _vp, ctypes.POINTER(bbtc_pl
 bbtc_plan_cuts = _sig("bbtc_plan_cuts", _st, _vp, _u32p)
 bbtc_plan_block = _sig("bbtc_plan_block", _st, _vp, _vp, c_u32, c_u32, _u32p, _u32p, _u32p, _u64p)
 bbtc_plan_to_host = _sig("bbtc_plan_to_host", _st, _vp, _vp)
+bbtc_plan_set_budget = _sig("bbtc_plan_set_budget", _st, _vp, c_u64)
 bbtc_plan_free = _sig("bbtc_plan_free", None, _vp)
 bbtc_n_tasks = _sig("bbtc_n_tasks", c_u64, c_u32)
 bbtc_task_index = _sig("bbtc_task_index", _st, c_u32, c_u32, c_u32, c_u32, _u64p)

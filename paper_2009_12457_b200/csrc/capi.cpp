@@ -224,25 +224,89 @@ struct Streamer {
     const BlockDesc& B = plan->blocks[b];
     return 4 * B.nnz * plan->edge_arenas().size() + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
   }
-  void issue(uint32_t b) {
-    if (issued[b]) return;
-    issued[b] = 1;
+  // Copies block b from the pinned host arenas to device arenas (edge arrays at
+  // edge offset e_dst, row offsets at ro_dst), then its ready flag = epoch.
+  void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst) {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+    auto arenas = plan->edge_arenas();
     if (B.nnz)
-      for (auto& A : plan->edge_arenas())
-        BBTC_CUDA(cudaMemcpyAsync(A.dev->p + B.e0, *A.host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
-    BBTC_CUDA(cudaMemcpyAsync(plan->rowptr.p + B.ro, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
-    if (epoch) {
-      // The ready flag is a 4-byte copy from pinned memory queued behind the block's
-      // copies: the copy engine writes it after the data, no SM involved.
-      plan->h_ready[b] = epoch;
-      BBTC_CUDA(cudaMemcpyAsync(plan->d_ready.p + b, plan->h_ready + b, 4, cudaMemcpyHostToDevice, cs));
-    }
-    BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+      for (size_t x = 0; x < arenas.size(); ++x)
+        BBTC_CUDA(cudaMemcpyAsync(dev_edges[x] + e_dst, *arenas[x].host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
+    BBTC_CUDA(cudaMemcpyAsync(dev_rowptr + ro_dst, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
+    flag(b, cs);
+    if (!ev[b]) BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     BBTC_CUDA(cudaEventRecord(ev[b], cs));
     bytes += block_bytes(b);
+  }
+  // The ready flag is a 4-byte copy from a read-only pinned table (h_epochs[e] = e)
+  // queued behind the block's copies: the copy engine writes it after the data.
+  void flag(uint32_t b, cudaStream_t cs) {
+    if (epoch)
+      BBTC_CUDA(cudaMemcpyAsync(plan->d_ready.p + b, plan->h_epochs + epoch, 4, cudaMemcpyHostToDevice, cs));
+  }
+  void issue(uint32_t b) {   // into the plan's full arenas, at the block's own offsets
+    if (issued[b]) return;
+    issued[b] = 1;
+    uint32_t* dev[3];
+    auto arenas = plan->edge_arenas();
+    for (size_t x = 0; x < arenas.size(); ++x) dev[x] = arenas[x].dev->p;
+    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro);
+  }
+};
+
+constexpr uint32_t kEpochs = 1u << 16;
+
+// Next ready-flag epoch of a plan (allocates the flags and the pinned epoch table on
+// first use; wraps by clearing the flags in stream order).
+static uint32_t next_epoch(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (!plan->h_epochs) {
+    BBTC_CUDA(cudaHostAlloc((void**)&plan->h_epochs, kEpochs * 4, cudaHostAllocPortable));
+    for (uint32_t e = 0; e < kEpochs; ++e) plan->h_epochs[e] = e;
+    plan->d_ready.alloc(plan->blocks.size(), ctx);
+    BBTC_CUDA(cudaMemsetAsync(plan->d_ready.p, 0, plan->blocks.size() * 4, ctx->stream));
+  }
+  if (++plan->epoch >= kEpochs) {
+    plan->epoch = 1;
+    BBTC_CUDA(cudaMemsetAsync(plan->d_ready.p, 0, plan->blocks.size() * 4, ctx->stream));
+  }
+  return plan->epoch;
+}
+
+// First-fit allocator over [0, cap) (the out-of-core cache arenas).
+struct RangeAlloc {
+  std::map<uint64_t, uint64_t> free_;   // offset -> length
+  explicit RangeAlloc(uint64_t cap) {
+    if (cap) free_[0] = cap;
+  }
+  bool alloc(uint64_t len, uint64_t* off) {
+    if (len == 0) { *off = 0; return true; }
+    for (auto it = free_.begin(); it != free_.end(); ++it)
+      if (it->second >= len) {
+        *off = it->first;
+        const uint64_t rest = it->second - len, at = it->first + len;
+        free_.erase(it);
+        if (rest) free_[at] = rest;
+        return true;
+      }
+    return false;
+  }
+  void release(uint64_t off, uint64_t len) {
+    if (len == 0) return;
+    auto it = free_.emplace(off, len).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
   }
 };
 
@@ -492,8 +556,15 @@ BBTC_API void bbtc_plan_free(bbtc_plan* plan) {
   if (plan->h_ccu) cudaFreeHost(plan->h_ccu);
   if (plan->h_ccv) cudaFreeHost(plan->h_ccv);
   if (plan->h_rowptr) cudaFreeHost(plan->h_rowptr);
-  if (plan->h_ready) cudaFreeHost(plan->h_ready);
+  if (plan->h_epochs) cudaFreeHost(plan->h_epochs);
   delete plan;
+}
+
+BBTC_API bbtc_status bbtc_plan_set_budget(bbtc_plan* plan, uint64_t bytes) {
+  return guard([&] {
+    if (!plan) raise(BBTC_EINVAL, "plan is NULL");
+    plan->budget = bytes;
+  });
 }
 
 BBTC_API uint64_t bbtc_n_tasks(uint32_t p) { return n_tasks(p); }
@@ -551,26 +622,27 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     count_zero(ctx, plan, d_counts.p);
     uint64_t h2d = 0;
     BBTC_CUDA(cudaEventRecord(k0, ctx->stream));
-    if (plan->resident) {
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), nullptr, 0);
-    } else {
-      // a6: every block is copied on the copy streams in first-use order and then
-      // flagged ready (epoch) on the device; ONE persistent count kernel runs
-      // concurrently and each warp waits on the flags of its item's three blocks,
-      // so the copies of later tasks overlap the intersections of earlier ones.
-      ensure_device_arenas(ctx, plan);
-      if (!plan->d_ready.p) {
-        BBTC_CUDA(cudaHostAlloc((void**)&plan->h_ready, plan->blocks.size() * 4, cudaHostAllocPortable));
-        plan->d_ready.alloc(plan->blocks.size(), ctx);
-        BBTC_CUDA(cudaMemsetAsync(plan->d_ready.p, 0, plan->blocks.size() * 4, ctx->stream));
-      }
-      const uint32_t epoch = ++plan->epoch;
-      // copies may start only after the flag reset above is ordered before them
+    // copy streams may only start after work already queued on the context stream
+    // (flag resets, the previous kernel that reads a cache region about to be reused)
+    auto copies_after_stream = [&] {
       cudaEvent_t go;
       BBTC_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
       BBTC_CUDA(cudaEventRecord(go, ctx->stream));
       for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, go, 0));
       cudaEventDestroy(go);
+    };
+    uint64_t all_bytes = 0;
+    for (uint32_t b = 0; b < plan->blocks.size(); ++b) all_bytes += Streamer(ctx, plan).block_bytes(b);
+    if (plan->resident) {
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), nullptr, 0);
+    } else if (plan->budget == 0 || plan->budget >= all_bytes) {
+      // a6: every block is copied on the copy streams in first-use order and then
+      // flagged ready (epoch) on the device; ONE persistent count kernel runs
+      // concurrently and each warp waits on the flags of its item's three blocks,
+      // so the copies of later tasks overlap the intersections of earlier ones.
+      ensure_device_arenas(ctx, plan);
+      const uint32_t epoch = next_epoch(ctx, plan);
+      copies_after_stream();
       Streamer s(ctx, plan);
       s.epoch = epoch;
       for (const TaskDesc& T : plan->tasks) {
@@ -584,6 +656,133 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         if (e) BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
       h2d = s.bytes;
       plan->resident = true;
+    } else {
+      // Out of core: the device holds at most `budget`
+      // bytes of blocks.  Tasks are cut, in execution order, into windows whose blocks
+      // fit the cache; per window, blocks no longer needed are evicted, the missing
+      // ones are copied into free cache space (first fit), every block of the window
+      // is flagged with the window's epoch, and the count kernel runs over the
+      // window's work items, its warps waiting on the flags as in the streamed mode.
+      auto arenas = plan->edge_arenas();
+      const uint64_t A = arenas.size();
+      const uint64_t ro_all = rowptr_len(plan);
+      const double frac_e = (double)(4 * A * plan->m) / (double)std::max<uint64_t>(all_bytes, 1);
+      const uint64_t cap_e = (uint64_t)((double)plan->budget * frac_e) / (4 * A);
+      const uint64_t cap_r = (plan->budget - cap_e * 4 * A) / 4;
+      std::vector<DevBuf<uint32_t>> cache(A);
+      for (auto& c : cache) c.alloc(std::max<uint64_t>(cap_e, 1), ctx);
+      DevBuf<uint32_t> cache_rp;
+      cache_rp.alloc(std::max<uint64_t>(std::min(cap_r, ro_all), 1), ctx);
+      uint32_t* dev_edges[3] = {cache[0].p, A > 1 ? cache[1].p : nullptr, A > 2 ? cache[2].p : nullptr};
+      RangeAlloc ea(cap_e), ra(cap_r);
+      const uint32_t nb = (uint32_t)plan->blocks.size();
+      std::vector<int64_t> at_e(nb, -1), at_r(nb, -1);   // cache placement of resident blocks
+      auto rlen = [&](uint32_t b) {
+        const BlockDesc& B = plan->blocks[b];
+        return (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+      };
+      std::vector<DevBuf<BlockDesc>> tables;   // per-window block tables, alive until the end
+      Streamer s(ctx, plan);
+      const size_t ne = plan->tasks.size();
+      size_t t0w = 0;
+      while (t0w < ne) {
+        // grow the window while its distinct blocks fit the cache
+        std::vector<char> inw(nb, 0);
+        std::vector<uint32_t> wblocks;
+        uint64_t we = 0, wr = 0;
+        size_t t1w = t0w;
+        for (; t1w < ne; ++t1w) {
+          const TaskDesc& T = plan->tasks[t1w];
+          uint64_t de = 0, dr = 0;
+          std::vector<uint32_t> add;
+          for (uint32_t b : {T.ij, T.ik, T.jk})
+            if (!inw[b] && std::find(add.begin(), add.end(), b) == add.end()) {
+              add.push_back(b);
+              de += plan->blocks[b].nnz;
+              dr += rlen(b);
+            }
+          if (we + de > cap_e || wr + dr > cap_r) break;
+          for (uint32_t b : add) {
+            inw[b] = 1;
+            wblocks.push_back(b);
+          }
+          we += de;
+          wr += dr;
+        }
+        if (t1w == t0w)
+          raise(BBTC_ERANGE, "device budget smaller than the three blocks of one task (raise it or p)");
+        // evict blocks the window does not use; place the missing ones
+        for (uint32_t b = 0; b < nb; ++b)
+          if (at_e[b] >= 0 && !inw[b]) {
+            ea.release(at_e[b], plan->blocks[b].nnz);
+            ra.release(at_r[b], rlen(b));
+            at_e[b] = at_r[b] = -1;
+          }
+        std::vector<uint32_t> load;
+        bool fits = true;
+        for (uint32_t b : wblocks)
+          if (at_e[b] < 0) {
+            uint64_t oe, orr;
+            if (!ea.alloc(plan->blocks[b].nnz, &oe) || !ra.alloc(rlen(b), &orr)) {
+              fits = false;
+              break;
+            }
+            at_e[b] = oe;
+            at_r[b] = orr;
+            load.push_back(b);
+          }
+        if (!fits) {   // fragmented: repack the whole window from scratch
+          ea = RangeAlloc(cap_e);
+          ra = RangeAlloc(cap_r);
+          std::fill(at_e.begin(), at_e.end(), -1);
+          std::fill(at_r.begin(), at_r.end(), -1);
+          load.clear();
+          for (uint32_t b : wblocks) {
+            uint64_t oe = 0, orr = 0;
+            ea.alloc(plan->blocks[b].nnz, &oe);
+            ra.alloc(rlen(b), &orr);
+            at_e[b] = oe;
+            at_r[b] = orr;
+            load.push_back(b);
+          }
+        }
+        // this window's block table: cache offsets of its blocks
+        std::vector<BlockDesc> tab = plan->blocks;
+        for (uint32_t b : wblocks) {
+          tab[b].e0 = (uint64_t)at_e[b];
+          tab[b].ro = (uint64_t)at_r[b];
+        }
+        tables.emplace_back();
+        tables.back().alloc(nb, ctx);
+        BBTC_CUDA(cudaMemcpyAsync(tables.back().p, tab.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice,
+                                  ctx->stream));
+        const uint32_t epoch = next_epoch(ctx, plan);
+        s.epoch = epoch;
+        copies_after_stream();   // the previous window's kernel is done with the reused space
+        for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b]);
+        for (uint32_t b : wblocks)
+          if (std::find(load.begin(), load.end(), b) == load.end())
+            s.flag(b, ctx->copy_streams[s.rr++ % ctx->copy_streams.size()]);
+        DevArenas ar;
+        ar.cols = dev_edges[0];
+        ar.it_u = plan->colmajor ? dev_edges[1] : dev_edges[1];
+        ar.it_v = plan->colmajor ? dev_edges[2] : dev_edges[0];
+        ar.rowptr = cache_rp.p;
+        ar.blocks = tables.back().p;
+        count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[t0w], plan->item_start[t1w],
+                     plan->d_ready.p, epoch, &ar);
+        t0w = t1w;
+      }
+      // the flags of the last window were written on the copy streams
+      for (auto cs : ctx->copy_streams) {
+        cudaEvent_t done;
+        BBTC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        BBTC_CUDA(cudaEventRecord(done, cs));
+        BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+        cudaEventDestroy(done);
+      }
+      h2d = s.bytes;
+      BBTC_CUDA(cudaStreamSynchronize(ctx->stream));   // caches and tables die with this scope
     }
     BBTC_CUDA(cudaEventRecord(k1, ctx->stream));
     std::vector<uint64_t> h(nt + 1);

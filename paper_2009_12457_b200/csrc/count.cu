@@ -382,7 +382,7 @@ void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts) {
 // Enqueues the count kernel over work items [item_lo, item_hi) of the plan's
 // execution order (this rank's residues only), accumulating into d_counts.
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
-                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch) {
+                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch, const DevArenas* ar) {
   cudaStream_t st = ctx->stream;
   const uint64_t nt = plan->info.n_tasks;
   if (item_hi <= item_lo + rank) return;
@@ -419,10 +419,17 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   }();
   const int per = std::max(1, std::min(per_sm[variant], cap_env > 0 ? cap_env : kCtasPerSm));
   const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
-  const uint32_t* iu = plan->colmajor ? plan->ccu.p : plan->rows.p;
-  const uint32_t* iv = plan->colmajor ? plan->ccv.p : plan->cols.p;
+  DevArenas own;
+  if (!ar) {   // the plan's own (fully resident) arenas
+    own.cols = plan->cols.p;
+    own.it_u = plan->colmajor ? plan->ccu.p : plan->rows.p;
+    own.it_v = plan->colmajor ? plan->ccv.p : plan->cols.p;
+    own.rowptr = plan->rowptr.p;
+    own.blocks = plan->d_blocks.p;
+    ar = &own;
+  }
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
-      plan->cols.p, iu, iv, plan->rowptr.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p,
+      ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, plan->d_tasks.p, plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
       (uint32_t)nt, ready, epoch);
   BBTC_LAUNCHED(ctx);

@@ -149,8 +149,9 @@ struct bbtc_plan {
   bbtc::DevBuf<TaskDesc> d_tasks;
   bbtc::DevBuf<uint64_t> d_item_start;
   bbtc::DevBuf<uint32_t> d_ready;     // streaming: per-block ready epoch
-  uint32_t* h_ready = nullptr;        // pinned source of the ready flags
+  uint32_t* h_epochs = nullptr;       // pinned, read-only: h_epochs[e] = e (source of the flag copies)
   uint32_t epoch = 0;
+  uint64_t budget = 0;                // out-of-core device budget in bytes (0 = unlimited)
   // pinned host copies (bbtc_plan_to_host)
   bool host_blocks = false;
   uint32_t* h_cols = nullptr;
@@ -181,9 +182,19 @@ void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* 
 void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,
                 bbtc_plan* plan);
 // count.cu
+// Where the count kernel finds the blocks: the plan's full arenas, or (out of core)
+// cache arenas holding a window's blocks at the offsets of a per-window block table.
+struct DevArenas {
+  const uint32_t* cols = nullptr;
+  const uint32_t* it_u = nullptr;
+  const uint32_t* it_v = nullptr;
+  const uint32_t* rowptr = nullptr;
+  const BlockDesc* blocks = nullptr;
+};
 void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
-                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch);
+                  uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch,
+                  const DevArenas* arenas = nullptr);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
 // capi.cpp (host)
 uint64_t n_tasks(uint32_t p);

@@ -222,3 +222,48 @@ def test_n_hint_does_not_matter_except_isolated(ctx, n_hint):
     s, d = inputs.rmat(10, 16, 7)
     og = oracle.OracleGraph(s, d, n_hint)
     check(ctx, s, d, n_hint, p=3, og=og)
+
+
+@pytest.mark.parametrize("frac", [0.25, 0.5, 0.9])
+@pytest.mark.parametrize("row_major", [False, True])
+def test_out_of_core_budget(ctx, frac, row_major):
+    """Host-resident plan counted with a device budget below the plan size."""
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(15, 16, 21)
+    og = oracle.OracleGraph(s, d, 1 << 15)
+    otot, opt, _, ocuts = og.count(8)
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 15)
+    plan = bb.Plan(ctx, g, 8, row_major=row_major)
+    total_bytes = plan.info()["block_bytes"]
+    plan.to_host()
+    plan.set_budget(int(total_bytes * frac))
+    for _ in range(2):   # twice: the second count reuses nothing (cache dies with the call)
+        tot, pt, tm = plan.count(timing=True)
+        assert tot == otot and np.array_equal(pt, opt)
+        assert tm["h2d_bytes"] >= total_bytes
+    plan.set_budget(1024)   # smaller than any task's blocks
+    with pytest.raises(bb.BBTCError):
+        plan.count()
+
+
+def test_hash_canonicalisation_option(gpu):
+    """BBTC_DEDUP=hash (hash-set canonicalisation) yields the same graph and counts."""
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import inputs, paper_2009_12457_b200 as bb; "
+            "s, d = inputs.rmat(14, 16, 3); s = np.concatenate([s, d[:999], s[:5]]); d = np.concatenate([d, s[:999], s[:5]]); "
+            "ctx = bb.Context(0); g = bb.Graph.from_edges(ctx, s, d, 1 << 14); p = bb.Plan(ctx, g, 5); "
+            "t, pt = p.count(); print(t, ','.join(map(str, pt)), g.stats()['m'])") % os.path.dirname(GOLD.rstrip('/golden'))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = code.replace(repr(os.path.dirname(GOLD.rstrip('/golden'))), repr(root))
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_DEDUP": "hash"},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    tot, pts, m = out.stdout.split()
+    s, d = inputs.rmat(14, 16, 3)
+    s2 = np.concatenate([s, d[:999], s[:5]])
+    d2 = np.concatenate([d, s[:999], s[:5]])
+    og = oracle.OracleGraph(s2, d2, 1 << 14)
+    otot, opt, _, _ = og.count(5)
+    assert int(tot) == otot and int(m) == og.m
+    assert [int(x) for x in pts.split(",")] == [int(x) for x in opt]
