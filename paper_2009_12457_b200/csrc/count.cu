@@ -28,7 +28,10 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr size_t kSmemBytes = (size_t)kWarps * (kTable * 4 + 32 * 16);
 constexpr int kCtasPerSm = 8;        // cap on resident CTAs per SM (BBTC_CTAS_PER_SM overrides)
-constexpr int kMinCtas = 5;          // register budget: >= 5 CTAs (40 warps) resident per SM
+#ifndef BBTC_MIN_CTAS
+#define BBTC_MIN_CTAS 5
+#endif
+constexpr int kMinCtas = BBTC_MIN_CTAS;   // register budget: >= 5 CTAs (40 warps) resident per SM
 constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
