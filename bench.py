@@ -296,12 +296,18 @@ def main():
     plan.to_host()
     tot_i, _, tm_i = plan.count(rank, world, timing=True)
     assert tot_x == tot_i
+    # Out of core: the device may hold only half of the blocks.
+    plan.unstage()
+    plan.set_budget(pinfo["block_bytes"] // 2)
+    tot_o, _, tm_o = plan.count(rank, world, timing=True)
+    assert tot_o == tot_x
     plan.close()
     g.close()
 
     peak, peak_src = load_peaks()
     b_alg_launch = pinfo["b_alg"] / world
     achieved = b_alg_launch / (kern / 1e3) / 1e9
+    traffic = ncu_traffic(cfg.name)
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -313,13 +319,19 @@ def main():
                 "h2d_bytes_per_step": 8 * E, "d2h_bytes_per_step": 8 * (nt + 1)},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(cfg.name), "kernel": "k_count", "kernel_ms": kern,
-                     "b_alg_bytes_per_launch": b_alg_launch, "peak_source": peak_src},
+                     "traffic": traffic, "kernel": "k_count", "kernel_ms": kern,
+                     "b_alg_bytes_per_launch": b_alg_launch, "peak_source": peak_src,
+                     "note": "achieved/frac are logical (B_alg = bytes Alg. 5 reads per edge, SURVEY 8(d)); the "
+                             "kernel reuses each staged list across a run of edges, so it can exceed 1. "
+                             "physical_frac = ncu DRAM bytes per launch / this kernel time / peak.",
+                     "physical_frac": (traffic / world / (kern / 1e3) / 1e9 / peak) if traffic else None},
         "clocks": clk.summary(),
         "triangles": tot,
         "breakdown_ms": {"step": ms, "count_kernel": kern, "prep_and_plan": ms - kern,
                          "count_excl_h2d": tm_x["t_total_ms"], "count_incl_h2d": tm_i["t_total_ms"],
-                         "h2d_bytes_blocks": tm_i["h2d_bytes"], "gen_s": t_gen},
+                         "h2d_bytes_blocks": tm_i["h2d_bytes"],
+                         "count_out_of_core_half_budget": tm_o["t_total_ms"], "h2d_bytes_out_of_core": tm_o["h2d_bytes"],
+                         "gen_s": t_gen},
         "plan": {"lambda": pinfo["lambda"], "dmax_blk": pinfo["dmax_blk"], "visits": pinfo["visits"],
                  "b_alg": pinfo["b_alg"], "work_items": pinfo["work_items"], "block_bytes": pinfo["block_bytes"]},
         "paper_context": "BBTC on 8xV100 DGX-1 hybrid, copy incl.: R-MAT scale24 1.154 s = 2.3e8 edges/s "

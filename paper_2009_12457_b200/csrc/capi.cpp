@@ -2,6 +2,7 @@
 // error mapping, contexts, task enumeration (Alg. 4), work items, the block
 // streamer (a6) and the synchronous count driver (Alg. 9's role).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstring>
 #include <numeric>
@@ -166,9 +167,23 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     const BlockDesc& B = plan->blocks[b];
     return 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
   };
-  for (uint32_t k = 0; k < p; ++k)
-    for (uint32_t j = 0; j <= k; ++j)
-      for (uint32_t i = 0; i <= j; ++i) {
+  // Execution order: "kji" (default: k outer, i inner — consecutive tasks share G_jk
+  // and walk G_ik) or "ijk" (Alg. 4's own order), BBTC_TASK_ORDER overrides.
+  std::vector<std::array<uint32_t, 3>> order;
+  order.reserve(n_tasks(p));
+  const char* oe = getenv("BBTC_TASK_ORDER");
+  if (oe && std::string(oe) == "ijk") {
+    for (uint32_t i = 0; i < p; ++i)
+      for (uint32_t j = i; j < p; ++j)
+        for (uint32_t k = j; k < p; ++k) order.push_back({i, j, k});
+  } else {
+    for (uint32_t k = 0; k < p; ++k)
+      for (uint32_t j = 0; j <= k; ++j)
+        for (uint32_t i = 0; i <= j; ++i) order.push_back({i, j, k});
+  }
+  for (const auto& ijk : order) {
+    const uint32_t i = ijk[0], j = ijk[1], k = ijk[2];
+    {
         TaskDesc T;
         T.ij = block_id(i, j);
         T.ik = block_id(i, k);
@@ -184,7 +199,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         uint64_t tb = bbytes(T.ij) + (T.ik != T.ij ? bbytes(T.ik) : 0) +
                       (T.jk != T.ij && T.jk != T.ik ? bbytes(T.jk) : 0);
         max_task_bytes = std::max(max_task_bytes, tb);
-      }
+    }
+  }
   plan->info.work_items = plan->item_start.back();
   plan->info.max_task_bytes = max_task_bytes;
   bbtc_ctx* ctx = plan->ctx;
@@ -682,6 +698,10 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         return (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
       };
       std::vector<DevBuf<BlockDesc>> tables;   // per-window block tables, alive until the end
+      std::vector<std::vector<uint32_t>> uses(nb);   // execution-order task indices using each block
+      for (uint32_t t = 0; t < plan->tasks.size(); ++t)
+        for (uint32_t b : {plan->tasks[t].ij, plan->tasks[t].ik, plan->tasks[t].jk})
+          if (uses[b].empty() || uses[b].back() != t) uses[b].push_back(t);
       Streamer s(ctx, plan);
       const size_t ne = plan->tasks.size();
       size_t t0w = 0;
@@ -711,26 +731,49 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         }
         if (t1w == t0w)
           raise(BBTC_ERANGE, "device budget smaller than the three blocks of one task (raise it or p)");
-        // evict blocks the window does not use; place the missing ones
-        for (uint32_t b = 0; b < nb; ++b)
-          if (at_e[b] >= 0 && !inw[b]) {
-            ea.release(at_e[b], plan->blocks[b].nnz);
-            ra.release(at_r[b], rlen(b));
-            at_e[b] = at_r[b] = -1;
-          }
+        // Place the window's missing blocks.  Resident blocks stay as long as there is
+        // room; when a block does not fit, the resident block outside the window whose
+        // next use lies farthest ahead is evicted (Belady: the task order is known).
+        auto next_use = [&](uint32_t b) -> size_t {
+          auto it = std::lower_bound(uses[b].begin(), uses[b].end(), (uint32_t)t1w);
+          return it == uses[b].end() ? SIZE_MAX : *it;
+        };
+        auto evict = [&](uint32_t b) {
+          ea.release(at_e[b], plan->blocks[b].nnz);
+          ra.release(at_r[b], rlen(b));
+          at_e[b] = at_r[b] = -1;
+        };
         std::vector<uint32_t> load;
         bool fits = true;
-        for (uint32_t b : wblocks)
-          if (at_e[b] < 0) {
-            uint64_t oe, orr;
-            if (!ea.alloc(plan->blocks[b].nnz, &oe) || !ra.alloc(rlen(b), &orr)) {
+        for (uint32_t b : wblocks) {
+          if (at_e[b] >= 0) continue;
+          uint64_t oe = 0, orr = 0;
+          for (;;) {
+            const bool ok_e = ea.alloc(plan->blocks[b].nnz, &oe);
+            const bool ok_r = ok_e && ra.alloc(rlen(b), &orr);
+            if (ok_r) break;
+            if (ok_e) ea.release(oe, plan->blocks[b].nnz);
+            int64_t victim = -1;
+            size_t far = 0;
+            for (uint32_t c = 0; c < nb; ++c)
+              if (at_e[c] >= 0 && !inw[c]) {
+                const size_t nu = next_use(c);
+                if (victim < 0 || nu > far) {
+                  victim = c;
+                  far = nu;
+                }
+              }
+            if (victim < 0) {
               fits = false;
               break;
             }
-            at_e[b] = oe;
-            at_r[b] = orr;
-            load.push_back(b);
+            evict((uint32_t)victim);
           }
+          if (!fits) break;
+          at_e[b] = oe;
+          at_r[b] = orr;
+          load.push_back(b);
+        }
         if (!fits) {   // fragmented: repack the whole window from scratch
           ea = RangeAlloc(cap_e);
           ra = RangeAlloc(cap_r);
