@@ -32,6 +32,10 @@ constexpr int kCtasPerSm = 8;        // cap on resident CTAs per SM (BBTC_CTAS_P
 #define BBTC_MIN_CTAS 5
 #endif
 constexpr int kMinCtas = BBTC_MIN_CTAS;   // register budget: >= 5 CTAs (40 warps) resident per SM
+#ifndef BBTC_PREFETCH
+#define BBTC_PREFETCH 1
+#endif
+constexpr bool kPrefetch = BBTC_PREFETCH;   // L2 prefetch of a batch's probe lists
 constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -274,6 +278,14 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       // edges whose staged list is empty cannot close a triangle: no probes for them
       const uint32_t bl = (in && alen > 0) ? blen : 0;
       const uint32_t bx = (uint32_t)BP.e0 + b0;   // index of P[0] in the cols arena
+      // Ask L2 for every lane's probe list now (fire-and-forget, no registers): the
+      // 32 random gathers of the batch then overlap the staging of S instead of each
+      // list's first round waiting out a full DRAM latency in turn.
+      if (kPrefetch && bl > 0) {
+        const uint32_t* pf = cols + bx;
+        const uint32_t lines = min((bl + 31) >> 5, 4u);
+        for (uint32_t x = 0; x < lines; ++x) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 32 * x));
+      }
       if (__any_sync(kFull, bl > 0)) {
         if (longl) {
           hits += long_list(cols, cS, __shfl_sync(kFull, a0, 0), __shfl_sync(kFull, alen, 0), bx, bl, tab, pay,
