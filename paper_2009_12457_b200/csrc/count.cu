@@ -370,21 +370,23 @@ __global__ void k_stats_edges(const uint32_t* __restrict__ it_v, const uint32_t*
 
 // Per block: nonempty rows R_ij and the largest partial degree.
 __global__ void k_stats_rows(const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks,
-                             const uint32_t* __restrict__ rows_per_block, unsigned long long* __restrict__ nonempty,
-                             uint32_t* __restrict__ dmax) {
-  const BlockDesc B = blocks[blockIdx.y];
-  const uint32_t nr = rows_per_block[blockIdx.y];
-  uint32_t ne = 0, mx = 0;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
-    uint32_t d = rowptr[B.ro + r + 1] - rowptr[B.ro + r];
-    ne += d > 0;
-    mx = max(mx, d);
-  }
-  ne = __reduce_add_sync(kFull, ne);
-  mx = __reduce_max_sync(kFull, mx);
-  if ((threadIdx.x & 31) == 0) {
-    if (ne) atomicAdd(&nonempty[blockIdx.y], (unsigned long long)ne);
-    atomicMax(dmax, mx);
+                             const uint32_t* __restrict__ rows_per_block, uint32_t nb,
+                             unsigned long long* __restrict__ nonempty, uint32_t* __restrict__ dmax) {
+  for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const BlockDesc B = blocks[b];
+    const uint32_t nr = rows_per_block[b];
+    uint32_t ne = 0, mx = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += gridDim.x * blockDim.x) {
+      uint32_t d = rowptr[B.ro + r + 1] - rowptr[B.ro + r];
+      ne += d > 0;
+      mx = max(mx, d);
+    }
+    ne = __reduce_add_sync(kFull, ne);
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31) == 0) {
+      if (ne) atomicAdd(&nonempty[b], (unsigned long long)ne);
+      atomicMax(dmax, mx);
+    }
   }
 }
 
@@ -479,8 +481,8 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_LAUNCHED(ctx);
   }
   if (nb) {
-    k_stats_rows<<<dim3(std::min((maxrows + 255) / 256, 64u), nb), 256, 0, st>>>(plan->rowptr.p, plan->d_blocks.p,
-                                                                                 rpb.p, nonempty.p, dmax.p);
+    k_stats_rows<<<dim3(std::min((maxrows + 255) / 256, 64u), std::min(nb, 16384u)), 256, 0, st>>>(
+        plan->rowptr.p, plan->d_blocks.p, rpb.p, nb, nonempty.p, dmax.p);
     BBTC_LAUNCHED(ctx);
   }
   std::vector<unsigned long long> h_ab(2 * ne), h_ne(nb);

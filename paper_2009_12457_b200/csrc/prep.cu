@@ -269,13 +269,15 @@ struct MinOp {
 };
 
 // Global -> block-local offsets.  grid.y walks the blocks.
-__global__ void k_row_local(const BlockDesc* __restrict__ blocks, const uint32_t* __restrict__ cuts,
+__global__ void k_row_local(const BlockDesc* __restrict__ blocks, uint32_t nb, const uint32_t* __restrict__ cuts,
                             uint32_t* __restrict__ rowptr) {
-  const BlockDesc B = blocks[blockIdx.y];
-  const uint32_t len = cuts[B.i + 1] - cuts[B.i] + 1;
-  const uint32_t base = (uint32_t)B.e0;
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < len; r += gridDim.x * blockDim.x)
-    rowptr[B.ro + r] -= base;
+  for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const BlockDesc B = blocks[b];
+    const uint32_t len = cuts[B.i + 1] - cuts[B.i] + 1;
+    const uint32_t base = (uint32_t)B.e0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < len; r += gridDim.x * blockDim.x)
+      rowptr[B.ro + r] -= base;
+  }
 }
 
 // Transpose keys: (block of edge e) << cb | local column.  Blocks are contiguous edge
@@ -614,8 +616,8 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   {
     uint32_t maxv = 0;
     for (uint32_t i = 0; i < pe; ++i) maxv = std::max(maxv, plan->cuts[i + 1] - plan->cuts[i] + 1);
-    dim3 grid(std::max(1u, std::min((maxv + kThreads - 1) / kThreads, 64u)), nb);
-    k_row_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dcuts.p, plan->rowptr.p);
+    dim3 grid(std::max(1u, std::min((maxv + kThreads - 1) / kThreads, 64u)), std::min(nb, 16384u));
+    k_row_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, nb, dcuts.p, plan->rowptr.p);
     BBTC_LAUNCHED(ctx);
   }
   tr.mark("rowptr");
@@ -630,7 +632,16 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     for (uint32_t j = 0; j < pe; ++j) maxw = std::max(maxw, plan->cuts[j + 1] - plan->cuts[j]);
     const int cb = std::max(1, bitlen(maxw - 1));
     const int kb = bitlen(nb - 1);
-    if (m && nb <= 36) {
+    // The batched path keeps every block's first edge in shared memory (8 B each).
+    const size_t key_smem = (size_t)nb * 8;
+    const bool batched = nb > 36 && key_smem <= 200 * 1024;
+    if (batched && key_smem > 48 * 1024) {
+      BBTC_CUDA(cudaFuncSetAttribute(k_transpose_keys<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)key_smem));
+      BBTC_CUDA(cudaFuncSetAttribute(k_transpose_keys<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)key_smem));
+    }
+    if (m && !batched) {
       // Few blocks: sort each block in place by its local column (no key pass).
       for (uint32_t b = 0; b < nb; ++b) {
         const BlockDesc& B = plan->blocks[b];

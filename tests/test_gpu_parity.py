@@ -267,3 +267,13 @@ def test_hash_canonicalisation_option(gpu):
     otot, opt, _, _ = og.count(5)
     assert int(tot) == otot and int(m) == og.m
     assert [int(x) for x in pts.split(",")] == [int(x) for x in opt]
+
+
+def test_many_parts(ctx):
+    """p = 100 (171,700 tasks, 5,050 blocks) and a user cut vector with many empty parts."""
+    s, d = inputs.rmat(13, 16, 12)
+    og = oracle.OracleGraph(s, d, 1 << 13)
+    check(ctx, s, d, 1 << 13, p=100, og=og)
+    rng = np.random.default_rng(3)
+    cuts = np.concatenate([[0], np.sort(rng.integers(0, og.n + 1, size=119)), [og.n]]).astype(np.uint32)
+    check(ctx, s, d, 1 << 13, cuts=cuts, og=og)
