@@ -377,6 +377,7 @@ BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out) 
       BBTC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
       c->copy_streams.push_back(s);
     }
+    BBTC_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
     // Keep freed pool memory cached between steps (no OS round trips per call).
     cudaMemPool_t pool;
     BBTC_CUDA(cudaDeviceGetDefaultMemPool(&pool, o.device));
@@ -394,6 +395,7 @@ BBTC_API void bbtc_ctx_free(bbtc_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto s : c->copy_streams) cudaStreamDestroy(s);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->cursor) cudaFree(c->cursor);
   for (auto& kv : c->cache) cudaFreeAsync(kv.second, c->stream);
   c->cache.clear();

@@ -89,6 +89,7 @@ struct bbtc_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::vector<cudaStream_t> copy_streams;
+  cudaStream_t aux_stream = nullptr;   // second compute stream (sorts overlapped with streaming)
   uint64_t launches = 0;
   int sm_count = 148;
   void* cursor = nullptr;          // device scratch: work-item cursors of the count kernel

@@ -342,6 +342,34 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(s, d, len, width, keys.p + c0, dmax.p);
     BBTC_LAUNCHED(ctx);
   };
+  // Stream-sort (host input): the canonical keys are radix-sorted in pieces on the
+  // aux stream while later pieces are still being copied host->device, then the
+  // sorted pieces are merged; the full sort no longer waits for the whole transfer.
+  // At most ~8 pieces (3 merge rounds), each a whole number of 32 Mi-pair copy chunks.
+  const uint64_t piece = std::max<uint64_t>(1ull << 26, ((E / 8 + (1ull << 25) - 1) >> 25) << 25);
+  bool stream_sort = !use_hash && mem == BBTC_MEM_HOST && E > piece && E < (1ull << 32) &&
+                     !getenv("BBTC_NO_STREAM_SORT");
+  DevBuf<uint64_t> alt;
+  DevBuf<uint8_t> sort_tmp;
+  size_t sort_tmp_bytes = 0;
+  struct Piece {
+    uint64_t off, len;
+    int sel;   // 0: sorted keys in `keys`, 1: in `alt`
+  };
+  std::vector<Piece> pieces;
+  if (stream_sort) {
+    alt.alloc(E, ctx);
+    cub::DoubleBuffer<uint64_t> db0(keys.p, alt.p);
+    BBTC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp_bytes, db0, piece, 0, 2 * bw, ctx->aux_stream));
+    sort_tmp.alloc(std::max<size_t>(sort_tmp_bytes, 1), ctx);
+  }
+  auto sort_piece = [&](uint64_t off, uint64_t len, int width) {
+    cub::DoubleBuffer<uint64_t> db(keys.p + off, alt.p + off);
+    size_t tb = sort_tmp_bytes;
+    BBTC_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, db, len, 0, 2 * width, ctx->aux_stream));
+    ctx->launches += radix_kernels(len, 2 * width);
+    pieces.push_back({off, len, db.selector});
+  };
   auto canon = [&](int width) {
     BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 8, st));
     if (use_hash) BBTC_CUDA(cudaMemsetAsync(table.p, 0xFF, (1ull << tbits) * 8, st));
@@ -362,6 +390,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       BBTC_CUDA(cudaEventCreateWithFlags(&ev_used[x], cudaEventDisableTiming));
       BBTC_CUDA(cudaEventRecord(ev_used[x], st));
     }
+    uint64_t sorted_upto = 0;   // stream-sort: keys [0, sorted_upto) handed to the aux stream
     for (uint64_t c0 = 0, it = 0; c0 < E; c0 += chunk, ++it) {
       const uint64_t len = std::min(chunk, E - c0);
       const int slot = it & 1;
@@ -372,6 +401,13 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
       launch_canon(ds.p + slot * chunk, dd.p + slot * chunk, len, c0, width);
       BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
+      // Stream-sort: once a sort piece is complete, sort it on the aux stream while
+      // the next pieces are still crossing PCIe.
+      if (stream_sort && (c0 + len - sorted_upto >= piece || c0 + len == E)) {
+        BBTC_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ev_used[slot], 0));
+        sort_piece(sorted_upto, c0 + len - sorted_upto, width);
+        sorted_upto = c0 + len;
+      }
     }
     for (int x = 0; x < 2; ++x) {
       cudaEventDestroy(ev_copied[x]);
@@ -384,7 +420,13 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
   BBTC_CUDA(cudaStreamSynchronize(st));
   if (E && bw < 32 && (max_id >> bw) != 0) {
-    // n_hint was too small for the ids: rebuild the keys at full width.
+    // n_hint was too small for the ids: rebuild the keys at full width (and sort
+    // them in one piece afterwards; the pieces sorted so far are void).
+    if (stream_sort) {
+      BBTC_CUDA(cudaStreamSynchronize(ctx->aux_stream));
+      stream_sort = false;
+      pieces.clear();
+    }
     bw = 32;
     canon(bw);
     BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
@@ -411,15 +453,58 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     table.reset();
     tr.mark("compact");
   } else if (E) {
-    DevBuf<uint64_t> alt;
-    alt.alloc(E, ctx);
-    cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
-    cub_call(ctx, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, bw + bid, st);
-    }, radix_kernels(E, bw + bid));
+    bool in_keys = true;   // where the fully sorted keys end up
+    if (stream_sort) {
+      // Join the aux stream, then merge the sorted pieces pairwise (log2 #pieces
+      // rounds of cub::DeviceMerge, ping-ponging between keys and alt).
+      cudaEvent_t joined;
+      BBTC_CUDA(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming));
+      BBTC_CUDA(cudaEventRecord(joined, ctx->aux_stream));
+      BBTC_CUDA(cudaStreamWaitEvent(st, joined, 0));
+      cudaEventDestroy(joined);
+      int sel = pieces[0].sel;
+      for (auto& pc : pieces)
+        if (pc.sel != sel) {
+          uint64_t* from = pc.sel ? alt.p : keys.p;
+          uint64_t* to = sel ? alt.p : keys.p;
+          BBTC_CUDA(cudaMemcpyAsync(to + pc.off, from + pc.off, pc.len * 8, cudaMemcpyDeviceToDevice, st));
+          pc.sel = sel;
+        }
+      std::vector<Piece> cur = pieces;
+      while (cur.size() > 1) {
+        uint64_t* from = sel ? alt.p : keys.p;
+        uint64_t* to = sel ? keys.p : alt.p;
+        std::vector<Piece> nxt;
+        for (size_t x = 0; x < cur.size(); x += 2) {
+          const Piece a = cur[x];
+          if (x + 1 < cur.size()) {
+            const Piece b = cur[x + 1];
+            cub_call(ctx, [&](void* t, size_t& tb) {
+              return cub::DeviceMerge::MergeKeys(t, tb, from + a.off, (int)a.len, from + b.off, (int)b.len,
+                                                 to + a.off, ::cuda::std::less<uint64_t>{}, st);
+            });
+            nxt.push_back({a.off, a.len + b.len, 1 - sel});
+          } else {
+            BBTC_CUDA(cudaMemcpyAsync(to + a.off, from + a.off, a.len * 8, cudaMemcpyDeviceToDevice, st));
+            nxt.push_back({a.off, a.len, 1 - sel});
+          }
+        }
+        cur.swap(nxt);
+        sel = 1 - sel;
+      }
+      in_keys = sel == 0;
+      sort_tmp.reset();
+    } else {
+      if (!alt.p) alt.alloc(E, ctx);
+      cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
+      cub_call(ctx, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, bw + bid, st);
+      }, radix_kernels(E, bw + bid));
+      in_keys = db.Current() == keys.p;
+    }
     tr.mark("sort1");
-    DevBuf<uint64_t>& sorted = db.Current() == keys.p ? keys : alt;
-    DevBuf<uint64_t>& other = db.Current() == keys.p ? alt : keys;
+    DevBuf<uint64_t>& sorted = in_keys ? keys : alt;
+    DevBuf<uint64_t>& other = in_keys ? alt : keys;
     DevBuf<uint64_t> nsel;
     nsel.alloc(1, ctx);
     cub_call(ctx, [&](void* t, size_t& b) {

@@ -277,3 +277,18 @@ def test_many_parts(ctx):
     rng = np.random.default_rng(3)
     cuts = np.concatenate([[0], np.sort(rng.integers(0, og.n + 1, size=119)), [og.n]]).astype(np.uint32)
     check(ctx, s, d, 1 << 13, cuts=cuts, og=og)
+
+
+def test_host_input_stream_sort(ctx):
+    """Host input large enough for the piecewise sort + merge path (> 2^26 raw pairs)."""
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(22, 20, 5)          # 83.9 M raw pairs -> 2 pieces
+    og = oracle.OracleGraph(s, d, 1 << 22)
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 22)
+    st = g.stats()
+    assert (st["n"], st["m"]) == (og.n, og.m)
+    assert np.array_equal(g.rank(), og.rank())
+    plan = bb.Plan(ctx, g, 6)
+    tot, pt = plan.count()
+    otot, opt, _, _ = og.count(cuts=plan.cuts())
+    assert tot == otot and np.array_equal(pt, opt)
