@@ -172,7 +172,19 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   std::vector<std::array<uint32_t, 3>> order;
   order.reserve(n_tasks(p));
   const char* oe = getenv("BBTC_TASK_ORDER");
-  if (oe && std::string(oe) == "ijk") {
+  const uint32_t h = plan->task_group;
+  if (h > 0 && h < p) {
+    // Out-of-core order: parts in groups of h; group triples (gi <= gj <= gk) one
+    // after the other, so a window holds the blocks between at most three groups
+    // (<= 3h^2 blocks) and consecutive windows share two of the three groups.
+    const uint32_t G = (p + h - 1) / h;
+    for (uint32_t gk = 0; gk < G; ++gk)
+      for (uint32_t gj = 0; gj <= gk; ++gj)
+        for (uint32_t gi = 0; gi <= gj; ++gi)
+          for (uint32_t k = gk * h; k < std::min(p, (gk + 1) * h); ++k)
+            for (uint32_t j = gj * h; j < std::min(k + 1, (gj + 1) * h); ++j)
+              for (uint32_t i = gi * h; i < std::min(j + 1, (gi + 1) * h); ++i) order.push_back({i, j, k});
+  } else if (oe && std::string(oe) == "ijk") {
     for (uint32_t i = 0; i < p; ++i)
       for (uint32_t j = i; j < p; ++j)
         for (uint32_t k = j; k < p; ++k) order.push_back({i, j, k});
@@ -291,35 +303,49 @@ static uint32_t next_epoch(bbtc_ctx* ctx, bbtc_plan* plan) {
 }
 
 // First-fit allocator over [0, cap) (the out-of-core cache arenas).
+// Every free range carries the last out-of-core window whose kernel read it (-1:
+// never read): a copy into it must wait for that kernel, and only for that one.
 struct RangeAlloc {
-  std::map<uint64_t, uint64_t> free_;   // offset -> length
+  struct Range {
+    uint64_t len;
+    int64_t reader;
+  };
+  std::map<uint64_t, Range> free_;   // offset -> range
   explicit RangeAlloc(uint64_t cap) {
-    if (cap) free_[0] = cap;
+    if (cap) free_[0] = {cap, -1};
   }
-  bool alloc(uint64_t len, uint64_t* off) {
-    if (len == 0) { *off = 0; return true; }
+  bool alloc(uint64_t len, uint64_t* off, int64_t* reader) {
+    if (len == 0) {
+      *off = 0;
+      *reader = -1;
+      return true;
+    }
     for (auto it = free_.begin(); it != free_.end(); ++it)
-      if (it->second >= len) {
+      if (it->second.len >= len) {
         *off = it->first;
-        const uint64_t rest = it->second - len, at = it->first + len;
+        *reader = it->second.reader;
+        const Range rest{it->second.len - len, it->second.reader};
+        const uint64_t at = it->first + len;
         free_.erase(it);
-        if (rest) free_[at] = rest;
+        if (rest.len) free_[at] = rest;
         return true;
       }
     return false;
   }
-  void release(uint64_t off, uint64_t len) {
+  void release(uint64_t off, uint64_t len, int64_t reader) {
     if (len == 0) return;
-    auto it = free_.emplace(off, len).first;
+    auto it = free_.emplace(off, Range{len, reader}).first;
     auto nx = std::next(it);
-    if (nx != free_.end() && it->first + it->second == nx->first) {
-      it->second += nx->second;
+    if (nx != free_.end() && it->first + it->second.len == nx->first) {
+      it->second.len += nx->second.len;
+      it->second.reader = std::max(it->second.reader, nx->second.reader);
       free_.erase(nx);
     }
     if (it != free_.begin()) {
       auto pv = std::prev(it);
-      if (pv->first + pv->second == it->first) {
-        pv->second += it->second;
+      if (pv->first + pv->second.len == it->first) {
+        pv->second.len += it->second.len;
+        pv->second.reader = std::max(pv->second.reader, it->second.reader);
         free_.erase(it);
       }
     }
@@ -582,6 +608,24 @@ BBTC_API bbtc_status bbtc_plan_set_budget(bbtc_plan* plan, uint64_t bytes) {
   return guard([&] {
     if (!plan) raise(BBTC_EINVAL, "plan is NULL");
     plan->budget = bytes;
+    // Below the plan's size, re-order the tasks in part groups sized so one group
+    // triple's blocks (<= 3h^2 of them) take about half the budget.
+    uint64_t all = 0;
+    Streamer sz(plan->ctx, plan);
+    for (uint32_t b = 0; b < plan->blocks.size(); ++b) all += sz.block_bytes(b);
+    uint32_t h = 0;
+    if (bytes > 0 && bytes < all && !plan->blocks.empty()) {
+      const double avg = (double)all / (double)plan->blocks.size();
+      const char* fe = getenv("BBTC_OOC_FILL");
+      const double fill = fe ? atof(fe) : 0.8;   // scripts/ooc_sweep.py: 0.8 moved the fewest bytes
+      h = (uint32_t)std::max(1.0, std::floor(std::sqrt(fill * (double)bytes / (3.0 * avg))));
+      if (h >= plan->p) h = 0;
+    }
+    if (h != plan->task_group) {
+      BBTC_CUDA(cudaStreamSynchronize(plan->ctx->stream));   // d_tasks may be in use
+      plan->task_group = h;
+      plan_tasks(plan, 1);
+    }
   });
 }
 
@@ -706,6 +750,10 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
           if (uses[b].empty() || uses[b].back() != t) uses[b].push_back(t);
       Streamer s(ctx, plan);
       const size_t ne = plan->tasks.size();
+      std::vector<int64_t> last_reader(nb, -1);   // last window whose kernel read each block
+      std::vector<cudaEvent_t> ev_done;           // per window: its kernel finished
+      next_epoch(ctx, plan);                       // (first use allocates and clears the flags)
+      copies_after_stream();                       // copies start after the flag reset
       size_t t0w = 0;
       while (t0w < ne) {
         // grow the window while its distinct blocks fit the cache
@@ -740,29 +788,38 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
           auto it = std::lower_bound(uses[b].begin(), uses[b].end(), (uint32_t)t1w);
           return it == uses[b].end() ? SIZE_MAX : *it;
         };
+        const int64_t w = (int64_t)ev_done.size();   // this window's index
         auto evict = [&](uint32_t b) {
-          ea.release(at_e[b], plan->blocks[b].nnz);
-          ra.release(at_r[b], rlen(b));
+          ea.release(at_e[b], plan->blocks[b].nnz, last_reader[b]);
+          ra.release(at_r[b], rlen(b), last_reader[b]);
           at_e[b] = at_r[b] = -1;
         };
+        // Copies of this window may overwrite space only after the kernels that last
+        // read it; victims the previous window did not read are preferred, so the
+        // copies usually overlap the previous window's kernel.
+        int64_t wait_for = -1;
         std::vector<uint32_t> load;
         bool fits = true;
         for (uint32_t b : wblocks) {
           if (at_e[b] >= 0) continue;
           uint64_t oe = 0, orr = 0;
+          int64_t te = -1, tr = -1;
           for (;;) {
-            const bool ok_e = ea.alloc(plan->blocks[b].nnz, &oe);
-            const bool ok_r = ok_e && ra.alloc(rlen(b), &orr);
+            const bool ok_e = ea.alloc(plan->blocks[b].nnz, &oe, &te);
+            const bool ok_r = ok_e && ra.alloc(rlen(b), &orr, &tr);
             if (ok_r) break;
-            if (ok_e) ea.release(oe, plan->blocks[b].nnz);
+            if (ok_e) ea.release(oe, plan->blocks[b].nnz, te);
             int64_t victim = -1;
             size_t far = 0;
+            bool recent = true;
             for (uint32_t c = 0; c < nb; ++c)
               if (at_e[c] >= 0 && !inw[c]) {
                 const size_t nu = next_use(c);
-                if (victim < 0 || nu > far) {
+                const bool rc = last_reader[c] >= w - 1;
+                if (victim < 0 || (recent && !rc) || (rc == recent && nu > far)) {
                   victim = c;
                   far = nu;
+                  recent = rc;
                 }
               }
             if (victim < 0) {
@@ -774,6 +831,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
           if (!fits) break;
           at_e[b] = oe;
           at_r[b] = orr;
+          wait_for = std::max(wait_for, std::max(te, tr));
           load.push_back(b);
         }
         if (!fits) {   // fragmented: repack the whole window from scratch
@@ -784,13 +842,16 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
           load.clear();
           for (uint32_t b : wblocks) {
             uint64_t oe = 0, orr = 0;
-            ea.alloc(plan->blocks[b].nnz, &oe);
-            ra.alloc(rlen(b), &orr);
+            int64_t tg = -1;
+            ea.alloc(plan->blocks[b].nnz, &oe, &tg);
+            ra.alloc(rlen(b), &orr, &tg);
             at_e[b] = oe;
             at_r[b] = orr;
             load.push_back(b);
           }
+          wait_for = w - 1;   // everything moved: after every earlier kernel
         }
+        for (uint32_t b : wblocks) last_reader[b] = w;
         // this window's block table: cache offsets of its blocks
         std::vector<BlockDesc> tab = plan->blocks;
         for (uint32_t b : wblocks) {
@@ -803,7 +864,8 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
                                   ctx->stream));
         const uint32_t epoch = next_epoch(ctx, plan);
         s.epoch = epoch;
-        copies_after_stream();   // the previous window's kernel is done with the reused space
+        if (wait_for >= 0)
+          for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, ev_done[wait_for], 0));
         for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b]);
         for (uint32_t b : wblocks)
           if (std::find(load.begin(), load.end(), b) == load.end())
@@ -816,8 +878,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         ar.blocks = tables.back().p;
         count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[t0w], plan->item_start[t1w],
                      plan->d_ready.p, epoch, &ar);
+        ev_done.emplace_back();
+        BBTC_CUDA(cudaEventCreateWithFlags(&ev_done.back(), cudaEventDisableTiming));
+        BBTC_CUDA(cudaEventRecord(ev_done.back(), ctx->stream));
         t0w = t1w;
       }
+      for (auto e : ev_done) cudaEventDestroy(e);   // destroyed events stay valid for queued waits
       // the flags of the last window were written on the copy streams
       for (auto cs : ctx->copy_streams) {
         cudaEvent_t done;

@@ -153,6 +153,7 @@ struct bbtc_plan {
   uint32_t* h_epochs = nullptr;       // pinned, read-only: h_epochs[e] = e (source of the flag copies)
   uint32_t epoch = 0;
   uint64_t budget = 0;                // out-of-core device budget in bytes (0 = unlimited)
+  uint32_t task_group = 0;            // task order: 0 = (k, j, i); h > 0 = groups of h parts (out of core)
   // pinned host copies (bbtc_plan_to_host)
   bool host_blocks = false;
   uint32_t* h_cols = nullptr;
