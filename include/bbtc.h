@@ -127,11 +127,19 @@ typedef struct {
   uint64_t work_items;      /* work items the count kernel schedules */
   uint64_t sum_a;           /* Σ_t Σ_(u,v)∈G_ij d(G_ik,u) (BBTC_PLAN_STATS) */
   uint64_t sum_b;           /* Σ_t Σ_(u,v)∈G_ij d(G_jk,v) (BBTC_PLAN_STATS) */
+  uint32_t dense_tasks;     /* tasks counted through bit rows over V_k (isDense) */
+  uint32_t dense_bits;      /* largest |V_k| a dense task may have (0 = dense path off) */
+  uint64_t dense_bytes;     /* device bytes of the bit rows (0 until the first resident count) */
 } bbtc_plan_info;
 
 #define BBTC_PLAN_STATS 1u     /* compute b_alg / visits / dmax_blk (one extra device pass) */
 #define BBTC_PLAN_ROWMAJOR 2u  /* walk G_ij row by row (stage N(G_ik,u), gather N(G_jk,v)) instead of
                                   the default column order (stage N(G_jk,v), gather N(G_ik,u)) */
+#define BBTC_PLAN_SPARSE 4u    /* no dense tasks: every task through the list kernel.  By default a
+                                  task whose V_k has at most BBTC_DENSE_BITS (env, default 2048)
+                                  vertices is counted on bit rows over V_k (Alg. 6's dense map,
+                                  P:552-572, chosen per task as isDense) while its
+                                  blocks are device-resident; same counts either way */
 
 /* a3-a5.  p: requested parts (>= 1; clamped to n).  cuts: NULL for the default
  * rule (R5: full-degree prefix rule) or a host array of p+1 entries

@@ -138,9 +138,10 @@ class Plan:
     """Cut vector + BCSR blocks + task list (bbtc_plan)."""
 
     def __init__(self, ctx: Context, graph: Graph, p: int = 1, cuts=None, stats: bool = False,
-                 row_major: bool = False):
+                 row_major: bool = False, sparse: bool = False):
         """row_major: walk each G_ij row by row (stage N(G_ik,u), gather N(G_jk,v)) instead of the
-        default column order (stage N(G_jk,v), gather N(G_ik,u)).  Same counts either way."""
+        default column order (stage N(G_jk,v), gather N(G_ik,u)).  sparse: no dense (bit-row)
+        tasks, every task through the list kernel.  Same counts either way."""
         self.ctx = ctx
         h = ctypes.c_void_p()
         cptr = None
@@ -148,7 +149,8 @@ class Plan:
             self._cuts_in = np.ascontiguousarray(cuts, dtype=np.uint32)
             p = len(self._cuts_in) - 1
             cptr = self._cuts_in.ctypes.data_as(L._u32p)
-        flags = (L.PLAN_STATS if stats else 0) | (L.PLAN_ROWMAJOR if row_major else 0)
+        flags = ((L.PLAN_STATS if stats else 0) | (L.PLAN_ROWMAJOR if row_major else 0)
+                 | (L.PLAN_SPARSE if sparse else 0))
         L.check(L.bbtc_plan_create(ctx.handle, graph._h, p, cptr, flags, ctypes.byref(h)))
         self._h = h
 

@@ -31,6 +31,7 @@ STATUS = {0: "BBTC_OK", -1: "BBTC_EINVAL", -2: "BBTC_ENOMEM", -3: "BBTC_EIO", -4
 MEM_HOST, MEM_DEVICE = 0, 1
 PLAN_STATS = 1
 PLAN_ROWMAJOR = 2
+PLAN_SPARSE = 4
 
 
 class BBTCError(RuntimeError):
@@ -52,7 +53,8 @@ class bbtc_plan_info(ctypes.Structure):
     _fields_ = [("p", c_u32), ("clamped", c_u32), ("n_tasks", c_u64), ("n_blocks", c_u64), ("m", c_u64),
                 ("m_max", c_u64), ("lambda_", ctypes.c_double), ("dmax_blk", c_u32), ("host_blocks", c_u32),
                 ("block_bytes", c_u64), ("max_task_bytes", c_u64), ("b_alg", c_u64), ("visits", c_u64),
-                ("work_items", c_u64), ("sum_a", c_u64), ("sum_b", c_u64)]
+                ("work_items", c_u64), ("sum_a", c_u64), ("sum_b", c_u64),
+                ("dense_tasks", c_u32), ("dense_bits", c_u32), ("dense_bytes", c_u64)]
 
 
 class bbtc_timing(ctypes.Structure):

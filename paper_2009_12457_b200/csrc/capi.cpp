@@ -193,6 +193,37 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
       for (uint32_t j = 0; j <= k; ++j)
         for (uint32_t i = 0; i <= j; ++i) order.push_back({i, j, k});
   }
+  // isDense: a task whose third part V_k is small enough for bit rows of
+  // at most kDenseMaxS words, and whose probe rows are long enough on average
+  // (delta(G_ik) >= BBTC_DENSE_RATIO x stride / 32) that reading a whole bit row
+  // beats walking the list.  Dense tasks go last (items [dense_item_lo, end)).
+  plan->dense_s.assign(p, 0);
+  plan->dense_ready = false;
+  plan->dense.reset();
+  static const double dense_ratio = [] {
+    const char* e = getenv("BBTC_DENSE_RATIO");
+    return e ? atof(e) : 0.0;
+  }();
+  if (plan->dense_bits && h == 0)
+    for (uint32_t k = 0; k < p; ++k) {
+      const uint32_t vk = plan->cuts[k + 1] - plan->cuts[k];
+      if (vk == 0 || vk > plan->dense_bits) continue;
+      uint32_t s = kDenseMinS;
+      while (s * 32 < vk) s <<= 1;
+      if (s <= kDenseMaxS) plan->dense_s[k] = s;
+    }
+  auto is_dense = [&](uint32_t i, uint32_t j, uint32_t k) {
+    const uint32_t s = plan->dense_s[k];
+    return s && plan->blocks[block_id(i, j)].nnz && delta(block_id(i, k)) >= dense_ratio * s / 32.0;
+  };
+  {
+    std::vector<std::array<uint32_t, 3>> sparse, dense;
+    for (const auto& t : order) (is_dense(t[0], t[1], t[2]) ? dense : sparse).push_back(t);
+    plan->dense_task_lo = (uint32_t)sparse.size();
+    order = sparse;
+    order.insert(order.end(), dense.begin(), dense.end());
+  }
+  plan->dense_item_lo = 0;
   for (const auto& ijk : order) {
     const uint32_t i = ijk[0], j = ijk[1], k = ijk[2];
     {
@@ -201,7 +232,11 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         T.ik = block_id(i, k);
         T.jk = block_id(j, k);
         T.idx = (uint32_t)task_index(p, i, j, k);
-        const double per_edge = 8.0 + delta(T.ik) + delta(T.jk);
+        if (plan->tasks.size() == plan->dense_task_lo) plan->dense_item_lo = plan->item_start.back();
+        T.pad = plan->tasks.size() >= plan->dense_task_lo ? plan->dense_s[k] : 0;
+        // A dense edge costs a fixed number of bit-row words; a list edge its lists.
+        const double per_edge = plan->tasks.size() >= plan->dense_task_lo ? 2.0 + plan->dense_s[k] / 8.0
+                                                                           : 8.0 + delta(T.ik) + delta(T.jk);
         uint64_t chunk = (uint64_t)(item_work / per_edge);
         chunk = std::max<uint64_t>(64, std::min<uint64_t>(1u << 16, (chunk + 31) / 32 * 32));
         T.chunk = (uint32_t)chunk;
@@ -213,8 +248,10 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         max_task_bytes = std::max(max_task_bytes, tb);
     }
   }
+  if (plan->dense_task_lo >= plan->tasks.size()) plan->dense_item_lo = plan->item_start.back();
   plan->info.work_items = plan->item_start.back();
   plan->info.max_task_bytes = max_task_bytes;
+  plan->info.dense_tasks = (uint32_t)(plan->tasks.size() - plan->dense_task_lo);
   bbtc_ctx* ctx = plan->ctx;
   plan->d_tasks.alloc(plan->tasks.size(), ctx);
   plan->d_item_start.alloc(plan->item_start.size(), ctx);
@@ -563,6 +600,8 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_CUDA(cudaStreamSynchronize(st));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
+    plan->dense.reset();
+    plan->dense_ready = false;
     plan->host_blocks = true;
     plan->resident = false;
     plan->info.host_blocks = 1;
@@ -588,6 +627,8 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
+    plan->dense.reset();
+    plan->dense_ready = false;
     plan->resident = false;
   });
 }
@@ -654,6 +695,14 @@ BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32
   });
 }
 
+// Resident blocks: the list kernel over the sparse tasks' items, then the bit-row
+// kernel over the dense tasks' items (building the bit rows on first use).
+static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts) {
+  dense_build(ctx, plan);
+  count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0);
+  count_launch_dense(ctx, plan, rank, world, d_counts, plan->dense_item_lo, plan->item_start.back());
+}
+
 BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
                                       uint64_t* d_counts) {
   return guard([&] {
@@ -661,7 +710,7 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
     if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
     if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident: call bbtc_stage or bbtc_count");
     count_zero(ctx, plan, d_counts);
-    count_launch(ctx, plan, rank, world, d_counts, 0, plan->item_start.back(), nullptr, 0);
+    count_resident(ctx, const_cast<bbtc_plan*>(plan), rank, world, d_counts);
   });
 }
 
@@ -696,7 +745,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     uint64_t all_bytes = 0;
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) all_bytes += Streamer(ctx, plan).block_bytes(b);
     if (plan->resident) {
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), nullptr, 0);
+      count_resident(ctx, plan, rank, world, d_counts.p);
     } else if (plan->budget == 0 || plan->budget >= all_bytes) {
       // a6: every block is copied on the copy streams in first-use order and then
       // flagged ready (epoch) on the device; ONE persistent count kernel runs

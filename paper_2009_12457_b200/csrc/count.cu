@@ -339,6 +339,125 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
   }
 }
 
+// ---- dense tasks (Alg. 6) ---------------------------------------------
+// Alg. 6 marks N(G_ik,u) in a dense map H over V_k and tests every w of N(G_jk,v)
+// against it.  When |V_k| is small, the B200 form of that map is a bit row: every
+// row y of a block (x,k) a dense task reads is kept as |V_k| bits (stride S words,
+// S a power of two), and an edge (u,v) of G_ij closes |row_ik(u) AND row_jk(v)|
+// triangles — S/4 uint4 loads and popcounts instead of a list walk, whatever the
+// list lengths.  k_dense_rows sets the bits from the block's edges.
+__global__ void k_dense_rows(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
+                             const BlockDesc* __restrict__ blocks, const uint32_t* __restrict__ ids, uint32_t n_ids,
+                             const uint64_t* __restrict__ off, const uint32_t* __restrict__ stride,
+                             uint32_t* __restrict__ dense) {
+  for (uint32_t y = blockIdx.y; y < n_ids; y += gridDim.y) {
+    const uint32_t b = ids[y];
+    const BlockDesc B = blocks[b];
+    uint32_t* D = dense + off[b];
+    const uint32_t S = stride[b];
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < B.nnz;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t u = it_u[B.e0 + x], w = it_v[B.e0 + x];
+      atomicOr(D + (uint64_t)u * S + (w >> 5), 1u << (w & 31));
+    }
+  }
+}
+
+// The edges [e_begin, e_end) of G_ij of one dense item, bit rows of stride S words:
+// 32 edges at a time; a round takes 32/LPR edges, LPR lanes per edge each loading Q
+// uint4 of both rows (kUnroll rounds of loads in flight).  Returns this lane's hits.
+template <int S>
+__device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
+                                                const uint32_t* __restrict__ Dik, const uint32_t* __restrict__ Djk,
+                                                uint64_t e_begin, uint64_t e_end, int lane) {
+  constexpr int kV = S / 4;                      // uint4 per row
+  constexpr int LPR = kV < 32 ? kV : 32;         // lanes per edge
+  constexpr int Q = kV / LPR;                    // uint4 per lane per row
+  constexpr int EPR = 32 / LPR;                  // edges per round
+  constexpr int kRounds = 32 / EPR;              // rounds per 32 edges
+  constexpr int kUnroll = kRounds < 4 / Q ? kRounds : 4 / Q;   // <= 4 uint4 of each row in flight
+  const int sub = lane / LPR, q = lane % LPR;
+  const uint4* Di = reinterpret_cast<const uint4*>(Dik) + q;
+  const uint4* Dj = reinterpret_cast<const uint4*>(Djk) + q;
+  uint32_t acc = 0;
+  for (uint64_t base = e_begin; base < e_end; base += 32) {
+    const uint64_t e = base + lane;
+    const bool valid = e < e_end;
+    const uint32_t u = valid ? it_u[e] : 0, v = valid ? it_v[e] : 0;
+    const int n = (int)(e_end - base < 32 ? e_end - base : 32);
+#pragma unroll
+    for (int r0 = 0; r0 < kRounds; r0 += kUnroll) {
+      if (r0 * EPR >= n) break;
+      uint4 a[kUnroll][Q], b[kUnroll][Q];
+#pragma unroll
+      for (int r = 0; r < kUnroll; ++r) {
+        const int idx = (r0 + r) * EPR + sub;
+        const uint32_t uu = __shfl_sync(kFull, u, idx & 31), vv = __shfl_sync(kFull, v, idx & 31);
+#pragma unroll
+        for (int x = 0; x < Q; ++x) {
+          if (idx < n) {
+            a[r][x] = Di[(uint64_t)uu * kV + x * LPR];
+            b[r][x] = Dj[(uint64_t)vv * kV + x * LPR];
+          } else {
+            a[r][x] = make_uint4(0, 0, 0, 0);
+            b[r][x] = a[r][x];
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kUnroll; ++r)
+#pragma unroll
+        for (int x = 0; x < Q; ++x)
+          acc += __popc(a[r][x].x & b[r][x].x) + __popc(a[r][x].y & b[r][x].y) + __popc(a[r][x].z & b[r][x].z) +
+                 __popc(a[r][x].w & b[r][x].w);
+    }
+  }
+  return acc;
+}
+
+// One warp per work item of a dense task (TaskDesc.pad = the bit-row stride of V_k).
+__global__ void __launch_bounds__(kWarps * 32, 4)
+k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
+              const uint32_t* __restrict__ dense, const uint64_t* __restrict__ off,
+              const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
+              const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
+              uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
+              unsigned long long* __restrict__ counts, uint32_t n_tasks) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(cursor, 1ull);
+    it = __shfl_sync(kFull, it, 0);
+    const uint64_t g = item_lo + it * world + rank;
+    if (g >= n_items) break;
+    uint32_t lo = 0, hi = n_exec - 1;
+    while (lo < hi) {
+      uint32_t mid = (lo + hi + 1) >> 1;
+      if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const TaskDesc T = tasks[lo];
+    const BlockDesc Bij = blocks[T.ij];
+    const uint32_t* Dik = dense + off[T.ik];
+    const uint32_t* Djk = dense + off[T.jk];
+    const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * T.chunk;
+    const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
+    uint32_t acc = 0;
+    switch (T.pad) {
+      case 8: acc = dense_edges<8>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 16: acc = dense_edges<16>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 32: acc = dense_edges<32>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 64: acc = dense_edges<64>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 128: acc = dense_edges<128>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      default: acc = dense_edges<256>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+    }
+    const uint32_t s = __reduce_add_sync(kFull, acc);
+    if (lane == 0 && s) {
+      atomicAdd(&counts[T.idx], (unsigned long long)s);
+      atomicAdd(&counts[n_tasks], (unsigned long long)s);
+    }
+  }
+}
+
 // ---- plan statistics (BBTC_PLAN_STATS): B_alg, visits, d'_max -------------------
 // Per task t and edge (u,v) of G_ij: a = d(G_ik,u), b = d(G_jk,v).
 // B_alg(t) = 4(|V_i|+1) + 8 R_ij + Σ (4 + 8 + 4a + 4b)
@@ -449,6 +568,67 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, plan->d_tasks.p, plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
       (uint32_t)nt, ready, epoch);
+  BBTC_LAUNCHED(ctx);
+}
+
+// Bit rows for every block (x,k) a dense task reads (as G_ik or G_jk): |V_x| rows of
+// dense_s[k] words.  Built once per resident plan, on the context stream.
+void dense_build(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (plan->dense_ready || plan->dense_task_lo >= plan->tasks.size()) return;
+  cudaStream_t st = ctx->stream;
+  const uint32_t nb = (uint32_t)plan->blocks.size();
+  std::vector<uint8_t> need(nb, 0);
+  for (size_t t = plan->dense_task_lo; t < plan->tasks.size(); ++t) need[plan->tasks[t].ik] = need[plan->tasks[t].jk] = 1;
+  plan->dense_off.assign(nb, 0);
+  std::vector<uint32_t> ids, stride(nb, 0);
+  uint64_t words = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    if (!need[b]) continue;
+    const BlockDesc& B = plan->blocks[b];
+    stride[b] = plan->dense_s[B.j];
+    plan->dense_off[b] = words;
+    words += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) * stride[b];
+    if (B.nnz) ids.push_back(b);
+  }
+  plan->dense.alloc(std::max<uint64_t>(words, 4), ctx);
+  plan->d_dense_off.alloc(nb, ctx);
+  DevBuf<uint32_t> d_ids, d_stride;
+  d_ids.alloc(std::max<size_t>(ids.size(), 1), ctx);
+  d_stride.alloc(nb, ctx);
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_dense_off.p, plan->dense_off.data(), nb * 8, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemcpyAsync(d_stride.p, stride.data(), nb * 4, cudaMemcpyHostToDevice, st));
+  if (!ids.empty()) BBTC_CUDA(cudaMemcpyAsync(d_ids.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemsetAsync(plan->dense.p, 0, words * 4, st));
+  if (!ids.empty()) {
+    const uint32_t* it_u = plan->colmajor ? plan->ccu.p : plan->rows.p;
+    const uint32_t* it_v = plan->colmajor ? plan->ccv.p : plan->cols.p;
+    k_dense_rows<<<dim3(64, std::min<uint32_t>((uint32_t)ids.size(), 16384u)), 256, 0, st>>>(
+        it_u, it_v, plan->d_blocks.p, d_ids.p, (uint32_t)ids.size(), plan->d_dense_off.p, d_stride.p, plan->dense.p);
+    BBTC_LAUNCHED(ctx);
+  }
+  // the host vectors above are read by async copies
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  plan->dense_ready = true;
+  plan->info.dense_bytes = words * 4;
+}
+
+void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
+                        uint64_t item_lo, uint64_t item_hi) {
+  cudaStream_t st = ctx->stream;
+  if (item_hi <= item_lo + rank) return;
+  if (!plan->dense_ready) raise(BBTC_ESTATE, "dense bit rows not built");
+  const uint64_t my_items = (item_hi - item_lo - rank + world - 1) / world;
+  if (!ctx->cursor) BBTC_CUDA(cudaMalloc((void**)&ctx->cursor, 8 * kCursorSlots));
+  unsigned long long* cursor = (unsigned long long*)ctx->cursor + (ctx->cursor_next++ % kCursorSlots);
+  BBTC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+  static int per_sm = 0;
+  if (!per_sm) BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_dense, kWarps * 32, 0));
+  const int per = std::max(1, std::min(per_sm, kCtasPerSm));
+  const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
+  k_count_dense<<<(unsigned)grid, kWarps * 32, 0, st>>>(
+      plan->colmajor ? plan->ccu.p : plan->rows.p, plan->colmajor ? plan->ccv.p : plan->cols.p, plan->dense.p,
+      plan->d_dense_off.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p, (uint32_t)plan->tasks.size(),
+      item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts, (uint32_t)plan->info.n_tasks);
   BBTC_LAUNCHED(ctx);
 }
 

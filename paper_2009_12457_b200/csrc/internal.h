@@ -99,6 +99,9 @@ struct bbtc_ctx {
   size_t cache_limit = 0;
 };
 constexpr int kCursorSlots = 1024;
+constexpr uint32_t kDenseMinS = 8;     // bit-row strides (words): powers of two in [8, 256]
+constexpr uint32_t kDenseMaxS = 256;
+constexpr uint32_t kDenseBitsDefault = 2048;
 
 struct bbtc_graph {
   bbtc_ctx* ctx = nullptr;
@@ -163,6 +166,18 @@ struct bbtc_plan {
   uint32_t* h_ccv = nullptr;
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;
+  // Dense tasks (Alg. 6's dense map over V_k, chosen per task as isDense,
+  // P:695-699): a part k with |V_k| <= dense_bits gets bit rows of stride dense_s[k]
+  // words (a power of two) for every block (x,k) a dense task reads; dense tasks run
+  // last in execution order, items [dense_item_lo, end), in k_count_dense.
+  uint32_t dense_bits = 0;            // largest |V_k| handled densely (0 = off)
+  std::vector<uint32_t> dense_s;      // per part: row stride in words (0 = sparse part)
+  uint64_t dense_item_lo = 0;         // first work item of the dense tasks (= end if none)
+  uint32_t dense_task_lo = 0;         // first dense task in execution order
+  bool dense_ready = false;           // bit rows built for the current arenas
+  bbtc::DevBuf<uint32_t> dense;       // bit rows of the blocks dense tasks read
+  std::vector<uint64_t> dense_off;    // per block: first word of its rows in `dense` (~0 = none)
+  bbtc::DevBuf<uint64_t> d_dense_off;
 
   // The per-edge u32 arenas the count kernel reads (all indexed by edge position):
   // cols (CSR lookups) + the iteration order arrays of the plan's mode.
@@ -198,6 +213,11 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
                   uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch,
                   const DevArenas* arenas = nullptr);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
+// Dense tasks: build the bit rows (once per resident plan) and count items
+// [item_lo, item_hi) of the dense tasks.
+void dense_build(bbtc_ctx* ctx, bbtc_plan* plan);
+void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
+                        uint64_t item_lo, uint64_t item_hi);
 // capi.cpp (host)
 uint64_t n_tasks(uint32_t p);
 uint64_t task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k);

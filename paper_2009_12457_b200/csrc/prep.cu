@@ -775,6 +775,12 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   plan->info.m_max = m_max;
   plan->info.lambda = m ? (double)m_max / (2.0 * (double)m / ((double)pe * (pe + 1))) : 0.0;
   plan->info.block_bytes = bytes;
+  {
+    const char* e = getenv("BBTC_DENSE_BITS");
+    plan->dense_bits = (flags & BBTC_PLAN_SPARSE) ? 0u : e ? (uint32_t)atoi(e) : kDenseBitsDefault;
+    plan->dense_bits = std::min(plan->dense_bits, kDenseMaxS * 32);
+    plan->info.dense_bits = plan->dense_bits;
+  }
   plan_tasks(plan, 1);
   tr.mark("tasks");
   if (flags & BBTC_PLAN_STATS) plan_stats(ctx, plan);

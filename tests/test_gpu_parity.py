@@ -292,3 +292,48 @@ def test_host_input_stream_sort(ctx):
     tot, pt = plan.count()
     otot, opt, _, _ = og.count(cuts=plan.cuts())
     assert tot == otot and np.array_equal(pt, opt)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_dense_and_sparse_tasks_agree(ctx, seed):
+    """isDense: bit-row tasks and list tasks give the oracle's counts."""
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(16, 16, seed)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 16)
+    for p in (2, 4, 8, 16):
+        otot, opt, _, _ = og.count(cuts=og.default_cuts(p))
+        dense = bb.Plan(ctx, g, p)
+        sparse = bb.Plan(ctx, g, p, sparse=True)
+        assert sparse.info()["dense_tasks"] == 0
+        assert dense.info()["dense_tasks"] > 0     # the top parts of R-MAT are small
+        for plan in (dense, sparse):
+            tot, pt = plan.count()
+            assert tot == otot and np.array_equal(pt, opt)
+        assert dense.info()["dense_bytes"] > 0
+
+
+def test_dense_strides(gpu):
+    """Bit rows of every stride (8..256 words): parts of 100..6000 vertices, dense up to 8192."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sizes = [6000, 3000, 1500, 700, 300, 100, 31, 1]
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); import inputs, paper_2009_12457_b200 as bb\n"
+        "s, d = inputs.rmat(15, 16, 4); ctx = bb.Context(0); g = bb.Graph.from_edges(ctx, s, d, 1 << 15)\n"
+        "n = g.stats()['n']; sizes = %r; cuts = [0, n - sum(sizes)]\n"
+        "for z in sizes: cuts.append(cuts[-1] + z)\n"
+        "p = bb.Plan(ctx, g, cuts=np.array(cuts, np.uint32)); t, pt = p.count()\n"
+        "t0, _ = p.count(0, 2); t1, _ = p.count(1, 2); assert t0 + t1 == t\n"
+        "print(t, ','.join(map(str, pt)), p.info()['dense_tasks'], ','.join(map(str, cuts)))\n") % (root, sizes)
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_DENSE_BITS": "8192"},
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    tot, pts, nd, cuts = out.stdout.split()
+    s, d = inputs.rmat(15, 16, 4)
+    og = oracle.OracleGraph(s, d, 1 << 15)
+    otot, opt, _, _ = og.count(cuts=np.array([int(x) for x in cuts.split(",")], np.uint32))
+    assert int(tot) == otot
+    assert [int(x) for x in pts.split(",")] == [int(x) for x in opt]
+    assert int(nd) > 60   # of 165 tasks: every one with k >= 1 and a non-empty G_ij
