@@ -299,13 +299,16 @@ def main():
     g = bb.Graph.from_edges(ctx, ds, dd, cfg.n_hint)
     plan = bb.Plan(ctx, g, p, stats=True)
     pinfo = plan.info()
+    plan.count(rank, world)                      # builds the dense tasks' bit rows
     tot_x, _, tm_x = plan.count(rank, world, timing=True)
+    dinfo = plan.info()
     plan.to_host()
     tot_i, _, tm_i = plan.count(rank, world, timing=True)
     assert tot_x == tot_i
     # Out of core: the device may hold only half of the blocks.
     plan.unstage()
     plan.set_budget(pinfo["block_bytes"] // 2)
+    plan.count(rank, world)                      # first use of the cache arenas' sizes
     tot_o, _, tm_o = plan.count(rank, world, timing=True)
     # The budget re-orders the tasks, so a rank's share of the items differs between
     # modes; the sums over ranks agree.
@@ -331,15 +334,20 @@ def main():
                 "h2d_bytes_per_step": 8 * E, "d2h_bytes_per_step": 8 * (nt + 1)},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_count", "kernel_ms": kern,
+                     "traffic": traffic, "kernel": "k_count + k_count_dense", "kernel_ms": kern,
                      "b_alg_bytes_per_launch": b_alg_launch, "peak_source": peak_src,
-                     "note": "achieved/frac are logical (B_alg = bytes Alg. 5 reads per edge, SURVEY 8(d)); the "
-                             "kernel reuses each staged list across a run of edges, so it can exceed 1. "
-                             "physical_frac = ncu DRAM bytes per launch / this kernel time / peak.",
+                     "note": "one count = the list kernel (k_count, sparse tasks) then the bit-row kernel "
+                             "(k_count_dense, dense tasks), timed together. achieved/frac are logical (B_alg = "
+                             "bytes Alg. 5 reads per edge, SURVEY 8(d)); staged lists reused across a run of "
+                             "edges and bit rows replacing long lists let it exceed 1. physical_frac = ncu DRAM "
+                             "bytes of both kernels per count / this time / peak.",
                      "physical_frac": (traffic / world / (kern / 1e3) / 1e9 / peak) if traffic else None},
         "clocks": clk.summary(),
         "triangles": tot,
         "breakdown_ms": {"step": ms, "count_kernel": kern, "prep_and_plan": ms - kern,
+                         "count_list_kernel": tm_x["t_kernel_ms"] - tm_x["t_dense_ms"],
+                         "count_dense_kernel": tm_x["t_dense_ms"], "dense_tasks": dinfo["dense_tasks"],
+                         "dense_bit_row_bytes": dinfo["dense_bytes"],
                          "count_excl_h2d": tm_x["t_total_ms"], "count_incl_h2d": tm_i["t_total_ms"],
                          "h2d_bytes_blocks": tm_i["h2d_bytes"],
                          "count_out_of_core_half_budget": tm_o["t_total_ms"], "h2d_bytes_out_of_core": tm_o["h2d_bytes"],

@@ -185,6 +185,7 @@ typedef struct {
   double t_kernel_ms;  /* device time of the count kernel(s) (CUDA events) */
   uint64_t h2d_bytes;  /* block bytes copied host->device by this call */
   uint64_t launches;   /* kernels launched by this call */
+  double t_dense_ms;   /* device time of the bit-row kernel (dense tasks) inside t_kernel_ms */
 } bbtc_timing;
 
 #define BBTC_COUNT_DEFAULT 0u

@@ -59,7 +59,7 @@ class bbtc_plan_info(ctypes.Structure):
 
 class bbtc_timing(ctypes.Structure):
     _fields_ = [("t_total_ms", ctypes.c_double), ("t_h2d_ms", ctypes.c_double), ("t_kernel_ms", ctypes.c_double),
-                ("h2d_bytes", c_u64), ("launches", c_u64)]
+                ("h2d_bytes", c_u64), ("launches", c_u64), ("t_dense_ms", ctypes.c_double)]
 
 
 def _sig(name, res, *args):

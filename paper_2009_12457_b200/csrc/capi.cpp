@@ -202,7 +202,7 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   plan->dense.reset();
   static const double dense_ratio = [] {
     const char* e = getenv("BBTC_DENSE_RATIO");
-    return e ? atof(e) : 0.0;
+    return e ? atof(e) : 1.0;   // scripts/dense_sweep.py: 0.5-2 equally fast on rmat24, 8x fewer bit-row bytes than 0
   }();
   if (plan->dense_bits && h == 0)
     for (uint32_t k = 0; k < p; ++k) {
@@ -234,9 +234,11 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         T.idx = (uint32_t)task_index(p, i, j, k);
         if (plan->tasks.size() == plan->dense_task_lo) plan->dense_item_lo = plan->item_start.back();
         T.pad = plan->tasks.size() >= plan->dense_task_lo ? plan->dense_s[k] : 0;
-        // A dense edge costs a fixed number of bit-row words; a list edge its lists.
-        const double per_edge = plan->tasks.size() >= plan->dense_task_lo ? 2.0 + plan->dense_s[k] / 8.0
-                                                                           : 8.0 + delta(T.ik) + delta(T.jk);
+        // A list edge costs its lists; a dense edge a fixed number of bit-row words.
+        // Dense tasks take the smaller of both chunks: without resident blocks (streamed,
+        // out of core) the list kernel runs them too.
+        double per_edge = 8.0 + delta(T.ik) + delta(T.jk);
+        if (plan->tasks.size() >= plan->dense_task_lo) per_edge = std::max(per_edge, 2.0 + plan->dense_s[k] / 8.0);
         uint64_t chunk = (uint64_t)(item_work / per_edge);
         chunk = std::max<uint64_t>(64, std::min<uint64_t>(1u << 16, (chunk + 31) / 32 * 32));
         T.chunk = (uint32_t)chunk;
@@ -697,9 +699,11 @@ BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32
 
 // Resident blocks: the list kernel over the sparse tasks' items, then the bit-row
 // kernel over the dense tasks' items (building the bit rows on first use).
-static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts) {
+static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
+                           cudaEvent_t mid = nullptr) {
   dense_build(ctx, plan);
   count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0);
+  if (mid) BBTC_CUDA(cudaEventRecord(mid, ctx->stream));
   count_launch_dense(ctx, plan, rank, world, d_counts, plan->dense_item_lo, plan->item_start.back());
 }
 
@@ -744,8 +748,10 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     };
     uint64_t all_bytes = 0;
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) all_bytes += Streamer(ctx, plan).block_bytes(b);
+    cudaEvent_t kmid = nullptr;
     if (plan->resident) {
-      count_resident(ctx, plan, rank, world, d_counts.p);
+      BBTC_CUDA(cudaEventCreate(&kmid));
+      count_resident(ctx, plan, rank, world, d_counts.p, kmid);
     } else if (plan->budget == 0 || plan->budget >= all_bytes) {
       // a6: every block is copied on the copy streams in first-use order and then
       // flagged ready (epoch) on the device; ONE persistent count kernel runs
@@ -950,8 +956,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     *total = h[nt];
     if (per_task) std::copy(h.begin(), h.begin() + nt, per_task);
-    float kms = 0;
+    float kms = 0, dms = 0;
     BBTC_CUDA(cudaEventElapsedTime(&kms, k0, k1));
+    if (kmid) {
+      BBTC_CUDA(cudaEventElapsedTime(&dms, kmid, k1));
+      cudaEventDestroy(kmid);
+    }
     cudaEventDestroy(k0);
     cudaEventDestroy(k1);
     if (tm) {
@@ -960,6 +970,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       tm->t_h2d_ms = 0;
       tm->h2d_bytes = h2d;
       tm->launches = ctx->launches - l0;
+      tm->t_dense_ms = dms;
     }
   });
 }

@@ -580,7 +580,10 @@ void dense_build(bbtc_ctx* ctx, bbtc_plan* plan) {
   std::vector<uint8_t> need(nb, 0);
   for (size_t t = plan->dense_task_lo; t < plan->tasks.size(); ++t) need[plan->tasks[t].ik] = need[plan->tasks[t].jk] = 1;
   plan->dense_off.assign(nb, 0);
-  std::vector<uint32_t> ids, stride(nb, 0);
+  std::vector<uint32_t>& ids = plan->dense_ids;
+  std::vector<uint32_t>& stride = plan->dense_stride;
+  ids.clear();
+  stride.assign(nb, 0);
   uint64_t words = 0;
   for (uint32_t b = 0; b < nb; ++b) {
     if (!need[b]) continue;
@@ -606,9 +609,7 @@ void dense_build(bbtc_ctx* ctx, bbtc_plan* plan) {
         it_u, it_v, plan->d_blocks.p, d_ids.p, (uint32_t)ids.size(), plan->d_dense_off.p, d_stride.p, plan->dense.p);
     BBTC_LAUNCHED(ctx);
   }
-  // the host vectors above are read by async copies
-  BBTC_CUDA(cudaStreamSynchronize(st));
-  plan->dense_ready = true;
+  plan->dense_ready = true;   // (the copies' host sources live in the plan)
   plan->info.dense_bytes = words * 4;
 }
 

@@ -177,6 +177,7 @@ struct bbtc_plan {
   bool dense_ready = false;           // bit rows built for the current arenas
   bbtc::DevBuf<uint32_t> dense;       // bit rows of the blocks dense tasks read
   std::vector<uint64_t> dense_off;    // per block: first word of its rows in `dense` (~0 = none)
+  std::vector<uint32_t> dense_ids, dense_stride;   // host sources of the build's async copies
   bbtc::DevBuf<uint64_t> d_dense_off;
 
   // The per-edge u32 arenas the count kernel reads (all indexed by edge position):

@@ -38,8 +38,16 @@ def sass_top(rep, top):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
-    data = rows[2:]
     ie, src, smp = h.index("Instructions Executed"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
+
+    def num(x):
+        try:
+            float(x or 0)
+            return True
+        except ValueError:
+            return False
+    # several kernels: their tables are concatenated (header rows repeat); pool the lines
+    data = [r for r in rows[2:] if len(r) > smp and num(r[smp])]
     tot = sum(float(r[smp] or 0) for r in data)
     order = sorted(range(len(data)), key=lambda i: -float(data[i][smp] or 0))[:top]
     return [{"idx": i, "sass": data[i][src].strip(), "inst": data[i][ie],
@@ -50,6 +58,22 @@ if __name__ == "__main__":
     rep = sys.argv[1]
     top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 25
     summary = {"report": rep, "launches": raw(rep), "top_stalls": sass_top(rep, top)}
+    if "--traffic" in sys.argv:
+        # profiles/ncu_count_<config>.json for bench.py: DRAM bytes of ONE count (the
+        # report must hold exactly one k_count and at most one k_count_dense launch).
+        cfg, out = sys.argv[sys.argv.index("--traffic") + 1: sys.argv.index("--traffic") + 3]
+        ks = [L for L in summary["launches"] if "k_count" in L["kernel"]]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        b = lambda L, k: float(L[k]) * scale[L[k + ".unit"]]  # noqa: E731
+        rd = sum(b(L, "dram__bytes_read.sum") for L in ks)
+        wr = sum(b(L, "dram__bytes_write.sum") for L in ks)
+        ms = sum(float(L["gpu__time_duration.sum"]) * (1e-3 if L["gpu__time_duration.sum.unit"] == "us" else 1)
+                 for L in ks)
+        with open(out, "w") as f:
+            json.dump({"config": cfg, "kernel": " + ".join(L["kernel"][:60] for L in ks), "source": rep,
+                       "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+                       "duration_ms_ncu": ms,
+                       "per_kernel": [{k: L[k] for k in L} for L in ks]}, f, indent=1)
     if "--json" in sys.argv:
         with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
             json.dump(summary, f, indent=1)
