@@ -50,8 +50,8 @@ typedef enum {
   BBTC_OK = 0,
   BBTC_EINVAL = -1,   /* bad argument (NULL handle, invalid cuts, p == 0 with no budget …) */
   BBTC_ENOMEM = -2,   /* device or host allocation failed */
-  BBTC_EIO = -3,      /* reserved (file input) */
-  BBTC_EPARSE = -4,   /* reserved (file input) */
+  BBTC_EIO = -3,      /* a file cannot be opened or read (bbtc_edges_read) */
+  BBTC_EPARSE = -4,   /* malformed input file; the message carries "path:line: what" */
   BBTC_ERANGE = -5,   /* a size does not fit the documented index widths */
   BBTC_ECUDA = -6,    /* CUDA runtime error (message carries cudaGetErrorString) */
   BBTC_ENCCL = -7,    /* reserved (collectives run in the caller's process group) */
@@ -107,6 +107,41 @@ BBTC_API bbtc_status bbtc_graph_rank(bbtc_ctx* ctx, const bbtc_graph* g, uint32_
  * sorted ascending.  For tests and inspection (it sorts on demand). */
 BBTC_API bbtc_status bbtc_graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col);
 BBTC_API void bbtc_graph_free(bbtc_graph* g);
+
+/* ------------------------------------------------------------- file input */
+/* The paper's input is a simple undirected graph given as an edge list (
+ * its datasets are Graph Challenge / SNAP edge files).  Formats:
+ *   BBTC_FMT_TEXT  one "u v" pair of 0-based decimal ids per line (tab, space or
+ *                  comma separated; further fields ignored); blank lines and lines
+ *                  starting with '#' or '%' are comments.
+ *   BBTC_FMT_MM    MatrixMarket coordinate file ("%%MatrixMarket matrix coordinate
+ *                  <field> <symmetry>", '%' comments, "rows cols nnz", then nnz
+ *                  1-based "i j [value]" lines; values ignored; n_hint = max(rows, cols)).
+ *   BBTC_FMT_BIN   little-endian uint32 pairs src0 dst0 src1 dst1 … (8 bytes per pair).
+ * No hygiene is applied: self-loops, duplicates and both orientations are passed on
+ * to bbtc_graph_from_edges, which drops / merges them (a1). */
+#define BBTC_FMT_TEXT 0
+#define BBTC_FMT_MM 1
+#define BBTC_FMT_BIN 2
+
+typedef struct {
+  uint32_t* src;      /* host, n_edges entries (library-allocated; release with bbtc_edges_free) */
+  uint32_t* dst;      /* host, n_edges entries */
+  uint64_t n_edges;   /* raw pairs read */
+  uint32_t n_hint;    /* vertex count the file declares (MatrixMarket), else 0 */
+  uint32_t reserved;
+} bbtc_edge_list;
+
+/* Host-only (no device needed): parses `path` into *out.  On error *out is empty.
+ * Errors: BBTC_EINVAL (NULL path/out, unknown format), BBTC_EIO (open/read
+ * failure), BBTC_EPARSE (malformed line — message "path:line: what"; a binary file
+ * whose size is not a multiple of 8), BBTC_ERANGE (an id > 0xFFFFFFFE), BBTC_ENOMEM. */
+BBTC_API bbtc_status bbtc_edges_read(const char* path, int format, bbtc_edge_list* out);
+BBTC_API void bbtc_edges_free(bbtc_edge_list* e);
+/* bbtc_edges_read followed by bbtc_graph_from_edges(…, max(n_hint, file's n_hint),
+ * BBTC_MEM_HOST, out).  Errors: those of both calls. */
+BBTC_API bbtc_status bbtc_graph_load(bbtc_ctx* ctx, const char* path, int format, uint32_t n_hint,
+                                     bbtc_graph** out);
 
 /* ------------------------------------------------------------------- plan */
 typedef struct {

@@ -18,7 +18,23 @@ import numpy as np
 from . import _lib as L
 from ._lib import BBTCError, MEM_DEVICE, MEM_HOST, PLAN_STATS
 
-__all__ = ["Context", "Graph", "Plan", "BBTCError", "n_tasks", "task_index", "task_ijk", "count_triangles"]
+__all__ = ["Context", "Graph", "Plan", "BBTCError", "n_tasks", "task_index", "task_ijk", "count_triangles",
+           "read_edges", "FORMATS"]
+
+FORMATS = {"text": L.FMT_TEXT, "mm": L.FMT_MM, "bin": L.FMT_BIN}
+
+
+def read_edges(path, fmt: str = "text"):
+    """bbtc_edges_read: (src, dst, n_hint) of an edge-list file (host only, no device)."""
+    e = L.bbtc_edge_list()
+    L.check(L.bbtc_edges_read(str(path).encode(), FORMATS[fmt], ctypes.byref(e)))
+    try:
+        n = e.n_edges
+        src = np.ctypeslib.as_array(e.src, shape=(n,)).copy() if n else np.empty(0, np.uint32)
+        dst = np.ctypeslib.as_array(e.dst, shape=(n,)).copy() if n else np.empty(0, np.uint32)
+        return src, dst, int(e.n_hint)
+    finally:
+        L.bbtc_edges_free(ctypes.byref(e))
 
 
 def _ptr(x, want_dtype):
@@ -98,6 +114,13 @@ class Graph:
         assert ps[2] == pd[2], "src and dst must both be host or both device"
         h = ctypes.c_void_p()
         L.check(L.bbtc_graph_from_edges(ctx.handle, ps[0], pd[0], ps[1], n_hint, ps[2], ctypes.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def load(cls, ctx: Context, path, fmt: str = "text", n_hint: int = 0) -> "Graph":
+        """bbtc_graph_load: read an edge-list file and build the graph (a1-a2)."""
+        h = ctypes.c_void_p()
+        L.check(L.bbtc_graph_load(ctx.handle, str(path).encode(), FORMATS[fmt], n_hint, ctypes.byref(h)))
         return cls(ctx, h)
 
     def stats(self) -> dict:

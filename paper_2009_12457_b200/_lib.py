@@ -32,6 +32,7 @@ MEM_HOST, MEM_DEVICE = 0, 1
 PLAN_STATS = 1
 PLAN_ROWMAJOR = 2
 PLAN_SPARSE = 4
+FMT_TEXT, FMT_MM, FMT_BIN = 0, 1, 2
 
 
 class BBTCError(RuntimeError):
@@ -57,6 +58,10 @@ class bbtc_plan_info(ctypes.Structure):
                 ("dense_tasks", c_u32), ("dense_bits", c_u32), ("dense_bytes", c_u64)]
 
 
+class bbtc_edge_list(ctypes.Structure):
+    _fields_ = [("src", _u32p), ("dst", _u32p), ("n_edges", c_u64), ("n_hint", c_u32), ("reserved", c_u32)]
+
+
 class bbtc_timing(ctypes.Structure):
     _fields_ = [("t_total_ms", ctypes.c_double), ("t_h2d_ms", ctypes.c_double), ("t_kernel_ms", ctypes.c_double),
                 ("h2d_bytes", c_u64), ("launches", c_u64), ("t_dense_ms", ctypes.c_double)]
@@ -79,6 +84,9 @@ bbtc_graph_stats_get = _sig("bbtc_graph_stats_get", _st, _vp, ctypes.POINTER(bbt
 bbtc_graph_rank = _sig("bbtc_graph_rank", _st, _vp, _vp, _u32p)
 bbtc_graph_csr = _sig("bbtc_graph_csr", _st, _vp, _vp, _u64p, _u32p)
 bbtc_graph_free = _sig("bbtc_graph_free", None, _vp)
+bbtc_edges_read = _sig("bbtc_edges_read", _st, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(bbtc_edge_list))
+bbtc_edges_free = _sig("bbtc_edges_free", None, ctypes.POINTER(bbtc_edge_list))
+bbtc_graph_load = _sig("bbtc_graph_load", _st, _vp, ctypes.c_char_p, ctypes.c_int, c_u32, _pp)
 bbtc_plan_create = _sig("bbtc_plan_create", _st, _vp, _vp, c_u32, _u32p, c_u32, _pp)
 bbtc_plan_info_get = _sig("bbtc_plan_info_get", _st, _vp, ctypes.POINTER(bbtc_plan_info))
 bbtc_plan_cuts = _sig("bbtc_plan_cuts", _st, _vp, _u32p)
