@@ -767,12 +767,21 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         s.issue(T.ik);
         s.issue(T.jk);
       }
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->item_start.back(), plan->d_ready.p, epoch);
+      // Sparse tasks first (they come first in execution order, so their blocks are
+      // issued first); the dense tasks' bit rows are built once every copy has landed
+      // and the bit-row kernel runs after the list kernel, as in the resident case.
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch);
       // the count stream must not run past copies it did not wait for
       for (auto& e : s.ev)
         if (e) BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
       h2d = s.bytes;
       plan->resident = true;
+      if (plan->dense_item_lo < plan->item_start.back()) {
+        BBTC_CUDA(cudaEventCreate(&kmid));
+        BBTC_CUDA(cudaEventRecord(kmid, ctx->stream));
+        dense_build(ctx, plan);
+        count_launch_dense(ctx, plan, rank, world, d_counts.p, plan->dense_item_lo, plan->item_start.back());
+      }
     } else {
       // Out of core: the device holds at most `budget`
       // bytes of blocks.  Tasks are cut, in execution order, into windows whose blocks

@@ -311,6 +311,15 @@ def test_dense_and_sparse_tasks_agree(ctx, seed):
             tot, pt = plan.count()
             assert tot == otot and np.array_equal(pt, opt)
         assert dense.info()["dense_bytes"] > 0
+        # streamed (a6): list kernel on the sparse tasks while blocks arrive, then the
+        # bit rows are built from the landed blocks and the dense tasks counted
+        dense.to_host()
+        tot, pt, tm = dense.count(timing=True)
+        assert tot == otot and np.array_equal(pt, opt)
+        assert tm["h2d_bytes"] > 0 and tm["t_dense_ms"] > 0 and dense.info()["dense_bytes"] > 0
+        dense.unstage()
+        tot, pt = dense.count()                     # streamed again after dropping the bit rows
+        assert tot == otot and np.array_equal(pt, opt)
 
 
 def test_dense_strides(gpu):
