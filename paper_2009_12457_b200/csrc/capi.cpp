@@ -188,6 +188,10 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     for (uint32_t i = 0; i < p; ++i)
       for (uint32_t j = i; j < p; ++j)
         for (uint32_t k = j; k < p; ++k) order.push_back({i, j, k});
+  } else if (oe && std::string(oe) == "kdesc") {
+    for (uint32_t k = p; k-- > 0;)
+      for (uint32_t j = 0; j <= k; ++j)
+        for (uint32_t i = 0; i <= j; ++i) order.push_back({i, j, k});
   } else {
     for (uint32_t k = 0; k < p; ++k)
       for (uint32_t j = 0; j <= k; ++j)
@@ -199,6 +203,7 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   // beats walking the list.  Dense tasks go last (items [dense_item_lo, end)).
   plan->dense_s.assign(p, 0);
   plan->dense_ready = false;
+  plan->s_ready = false;
   plan->dense.reset();
   static const double dense_ratio = [] {
     const char* e = getenv("BBTC_DENSE_RATIO");
@@ -697,6 +702,82 @@ BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32
   });
 }
 
+// Streaming order (a6): the sparse tasks reordered so that the blocks copied first
+// unlock the most work.  Greedy: every task whose blocks are all issued goes next (in
+// execution order); otherwise the task with the most work (work items, which carry
+// equal estimated work, R8) per byte of its blocks still to copy.  The copies follow
+// the same order, so the kernel always has unlocked work while later blocks are in
+// flight (the execution order puts the densest column of blocks last: with it the
+// kernel idles until those copies land).  O(T^2): plans with more than kGreedyMax
+// sparse tasks keep the execution order.
+static void stream_order(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (plan->s_ready) return;
+  constexpr size_t kGreedyMax = 6000;
+  const size_t ns = plan->dense_task_lo;
+  std::vector<uint32_t> ord;
+  ord.reserve(ns);
+  if (ns <= kGreedyMax) {
+    const uint32_t nb = (uint32_t)plan->blocks.size();
+    std::vector<double> bytes(nb);
+    for (uint32_t b = 0; b < nb; ++b) bytes[b] = (double)Streamer(ctx, plan).block_bytes(b);
+    std::vector<char> have(nb, 0), done(ns, 0);
+    size_t left = ns;
+    while (left) {
+      bool took = false;
+      for (size_t t = 0; t < ns; ++t) {
+        if (done[t]) continue;
+        const TaskDesc& T = plan->tasks[t];
+        if (have[T.ij] && have[T.ik] && have[T.jk]) {
+          done[t] = 1;
+          --left;
+          ord.push_back((uint32_t)t);
+          took = true;
+        }
+      }
+      if (took) continue;
+      double best = -1;
+      size_t bt = 0;
+      for (size_t t = 0; t < ns; ++t) {
+        if (done[t]) continue;
+        const TaskDesc& T = plan->tasks[t];
+        double miss = 0;
+        if (!have[T.ij]) miss += bytes[T.ij];
+        if (!have[T.ik] && T.ik != T.ij) miss += bytes[T.ik];
+        if (!have[T.jk] && T.jk != T.ij && T.jk != T.ik) miss += bytes[T.jk];
+        const double work = (double)(plan->item_start[t + 1] - plan->item_start[t]);
+        const double score = work / std::max(miss, 1.0);
+        if (score > best) {
+          best = score;
+          bt = t;
+        }
+      }
+      const TaskDesc& T = plan->tasks[bt];
+      have[T.ij] = have[T.ik] = have[T.jk] = 1;
+    }
+  } else {
+    for (size_t t = 0; t < ns; ++t) ord.push_back((uint32_t)t);
+  }
+  plan->s_tasks.clear();
+  plan->s_item_start.assign(1, 0);
+  for (uint32_t t : ord) {
+    plan->s_tasks.push_back(plan->tasks[t]);
+    plan->s_item_start.push_back(plan->s_item_start.back() + plan->item_start[t + 1] - plan->item_start[t]);
+  }
+  // the dense tasks keep their place after the sparse ones (items [dense_item_lo, end))
+  for (size_t t = ns; t < plan->tasks.size(); ++t) {
+    plan->s_tasks.push_back(plan->tasks[t]);
+    plan->s_item_start.push_back(plan->s_item_start.back() + plan->item_start[t + 1] - plan->item_start[t]);
+  }
+  plan->d_s_tasks.alloc(std::max<size_t>(plan->s_tasks.size(), 1), ctx);
+  plan->d_s_item_start.alloc(plan->s_item_start.size(), ctx);
+  if (!plan->s_tasks.empty())
+    BBTC_CUDA(cudaMemcpyAsync(plan->d_s_tasks.p, plan->s_tasks.data(), plan->s_tasks.size() * sizeof(TaskDesc),
+                              cudaMemcpyHostToDevice, ctx->stream));
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_s_item_start.p, plan->s_item_start.data(), plan->s_item_start.size() * 8,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  plan->s_ready = true;
+}
+
 // Resident blocks: the list kernel over the sparse tasks' items, then the bit-row
 // kernel over the dense tasks' items (building the bit rows on first use).
 static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
@@ -746,6 +827,15 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, go, 0));
       cudaEventDestroy(go);
     };
+    // t_h2d_ms: from the start of the call to the end of the last copy (events on the copy streams)
+    std::vector<cudaEvent_t> c_end;
+    auto copies_done = [&] {
+      for (auto cs : ctx->copy_streams) {
+        c_end.emplace_back();
+        BBTC_CUDA(cudaEventCreate(&c_end.back()));
+        BBTC_CUDA(cudaEventRecord(c_end.back(), cs));
+      }
+    };
     uint64_t all_bytes = 0;
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) all_bytes += Streamer(ctx, plan).block_bytes(b);
     cudaEvent_t kmid = nullptr;
@@ -760,9 +850,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       ensure_device_arenas(ctx, plan);
       const uint32_t epoch = next_epoch(ctx, plan);
       copies_after_stream();
+      const char* so = getenv("BBTC_STREAM_ORDER");
+      const bool greedy = !(so && std::string(so) == "exec");
+      if (greedy) stream_order(ctx, plan);
       Streamer s(ctx, plan);
       s.epoch = epoch;
-      for (const TaskDesc& T : plan->tasks) {
+      for (const TaskDesc& T : greedy ? plan->s_tasks : plan->tasks) {
         s.issue(T.ij);
         s.issue(T.ik);
         s.issue(T.jk);
@@ -770,11 +863,13 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       // Sparse tasks first (they come first in execution order, so their blocks are
       // issued first); the dense tasks' bit rows are built once every copy has landed
       // and the bit-row kernel runs after the list kernel, as in the resident case.
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch);
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch, nullptr,
+                   greedy ? plan->d_s_tasks.p : nullptr, greedy ? plan->d_s_item_start.p : nullptr);
       // the count stream must not run past copies it did not wait for
       for (auto& e : s.ev)
         if (e) BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
       h2d = s.bytes;
+      copies_done();
       plan->resident = true;
       if (plan->dense_item_lo < plan->item_start.back()) {
         BBTC_CUDA(cudaEventCreate(&kmid));
@@ -957,6 +1052,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         cudaEventDestroy(done);
       }
       h2d = s.bytes;
+      copies_done();
       BBTC_CUDA(cudaStreamSynchronize(ctx->stream));   // caches and tables die with this scope
     }
     BBTC_CUDA(cudaEventRecord(k1, ctx->stream));
@@ -971,16 +1067,22 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       BBTC_CUDA(cudaEventElapsedTime(&dms, kmid, k1));
       cudaEventDestroy(kmid);
     }
-    cudaEventDestroy(k0);
-    cudaEventDestroy(k1);
     if (tm) {
       tm->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       tm->t_kernel_ms = kms;
       tm->t_h2d_ms = 0;
+      for (auto e : c_end) {
+        float ms = 0;
+        BBTC_CUDA(cudaEventElapsedTime(&ms, k0, e));
+        tm->t_h2d_ms = std::max(tm->t_h2d_ms, (double)ms);
+      }
       tm->h2d_bytes = h2d;
       tm->launches = ctx->launches - l0;
       tm->t_dense_ms = dms;
     }
+    for (auto e : c_end) cudaEventDestroy(e);
+    cudaEventDestroy(k0);
+    cudaEventDestroy(k1);
   });
 }
 

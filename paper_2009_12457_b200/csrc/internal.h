@@ -179,6 +179,13 @@ struct bbtc_plan {
   std::vector<uint64_t> dense_off;    // per block: first word of its rows in `dense` (~0 = none)
   std::vector<uint32_t> dense_ids, dense_stride;   // host sources of the build's async copies
   bbtc::DevBuf<uint64_t> d_dense_off;
+  // Streamed counts (a6): the sparse tasks in block-unlock order (greedy most work per
+  // byte still to copy), so the kernel has work while later blocks are in flight.
+  bool s_ready = false;
+  std::vector<TaskDesc> s_tasks;
+  std::vector<uint64_t> s_item_start;
+  bbtc::DevBuf<TaskDesc> d_s_tasks;
+  bbtc::DevBuf<uint64_t> d_s_item_start;
 
   // The per-edge u32 arenas the count kernel reads (all indexed by edge position):
   // cols (CSR lookups) + the iteration order arrays of the plan's mode.
@@ -212,7 +219,8 @@ struct DevArenas {
 void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                   uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch,
-                  const DevArenas* arenas = nullptr);
+                  const DevArenas* arenas = nullptr, const TaskDesc* tasks = nullptr,
+                  const uint64_t* item_start = nullptr);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
 // Dense tasks: build the bit rows (once per resident plan) and count items
 // [item_lo, item_hi) of the dense tasks.
