@@ -304,18 +304,17 @@ def main():
     dinfo = plan.info()
     plan.to_host()
     tot_i, _, tm_i = plan.count(rank, world, timing=True)
-    assert tot_x == tot_i
     # Out of core: the device may hold only half of the blocks.
     plan.unstage()
     plan.set_budget(pinfo["block_bytes"] // 2)
     plan.count(rank, world)                      # first use of the cache arenas' sizes
     tot_o, _, tm_o = plan.count(rank, world, timing=True)
-    # The budget re-orders the tasks, so a rank's share of the items differs between
-    # modes; the sums over ranks agree.
-    sums = torch.tensor([tot_x, tot_o], dtype=torch.int64, device="cuda")
+    # Streaming (unlock order) and the budget re-order the tasks, so a rank's share of
+    # the items differs between modes; the sums over ranks agree.
+    sums = torch.tensor([tot_x, tot_i, tot_o], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(sums)
-    assert int(sums[0]) == int(sums[1]) == tot
+    assert int(sums[0]) == int(sums[1]) == int(sums[2]) == tot
     plan.close()
     g.close()
 

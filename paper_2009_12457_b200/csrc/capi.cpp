@@ -298,19 +298,33 @@ struct Streamer {
   }
   // Copies block b from the pinned host arenas to device arenas (edge arrays at
   // edge offset e_dst, row offsets at ro_dst), then its ready flag = epoch.
-  void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst) {
+  // expand: ship a column-major block's column ids as its column offsets (|V_j|+1
+  // words instead of nnz: 8 instead of 12 bytes per edge) and expand them into the
+  // device ccv on the copy stream, before the ready flag.
+  void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst,
+            bool expand = false) {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
     auto arenas = plan->edge_arenas();
+    expand = expand && plan->colmajor && plan->h_colptr && plan->colptr.p;
+    const size_t direct = expand ? 2 : arenas.size();   // arena 2 (ccv) comes from the offsets
     if (B.nnz)
-      for (size_t x = 0; x < arenas.size(); ++x)
+      for (size_t x = 0; x < direct; ++x)
         BBTC_CUDA(cudaMemcpyAsync(dev_edges[x] + e_dst, *arenas[x].host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
+    if (expand && B.nnz) {
+      const uint32_t ncols = plan->cuts[B.j + 1] - plan->cuts[B.j];
+      BBTC_CUDA(cudaMemcpyAsync(plan->colptr.p + plan->co_off[b], plan->h_colptr + plan->co_off[b],
+                                ((uint64_t)ncols + 1) * 4, cudaMemcpyHostToDevice, cs));
+      colptr_expand(cs, plan->colptr.p + plan->co_off[b], ncols, dev_edges[2] + e_dst);
+      ctx->launches++;
+      bytes += ((uint64_t)ncols + 1) * 4;
+    }
     BBTC_CUDA(cudaMemcpyAsync(dev_rowptr + ro_dst, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
     flag(b, cs);
     if (!ev[b]) BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     BBTC_CUDA(cudaEventRecord(ev[b], cs));
-    bytes += block_bytes(b);
+    bytes += block_bytes(b) - (direct < arenas.size() ? 4 * B.nnz : 0);
   }
   // The ready flag is a 4-byte copy from a read-only pinned table (h_epochs[e] = e)
   // queued behind the block's copies: the copy engine writes it after the data.
@@ -324,7 +338,7 @@ struct Streamer {
     uint32_t* dev[3];
     auto arenas = plan->edge_arenas();
     for (size_t x = 0; x < arenas.size(); ++x) dev[x] = arenas[x].dev->p;
-    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro);
+    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro, !getenv("BBTC_NO_COLPTR"));
   }
 };
 
@@ -404,6 +418,7 @@ static uint64_t rowptr_len(const bbtc_plan* plan) {
 
 static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
   if (!plan->rowptr.p) plan->rowptr.alloc(rowptr_len(plan), ctx);
+  if (plan->h_colptr && !plan->colptr.p) plan->colptr.alloc(std::max<uint64_t>(plan->co_off.back(), 1), ctx);
   for (auto& A : plan->edge_arenas())
     if (!A.dev->p && plan->m) A.dev->alloc(plan->m, ctx);
 }
@@ -604,6 +619,13 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     }
     BBTC_CUDA(cudaHostAlloc((void**)&plan->h_rowptr, std::max<uint64_t>(ro, 1) * 4, cudaHostAllocPortable));
     BBTC_CUDA(cudaMemcpyAsync(plan->h_rowptr, plan->rowptr.p, ro * 4, cudaMemcpyDeviceToHost, st));
+    if (plan->colmajor) {   // the streamed form of ccv: per-block column offsets
+      DevBuf<uint32_t> cp;
+      const uint64_t len = colptr_build(ctx, plan, &cp);
+      BBTC_CUDA(cudaHostAlloc((void**)&plan->h_colptr, std::max<uint64_t>(len, 1) * 4, cudaHostAllocPortable));
+      BBTC_CUDA(cudaMemcpyAsync(plan->h_colptr, cp.p, len * 4, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaStreamSynchronize(st));
+    }
     BBTC_CUDA(cudaStreamSynchronize(st));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
@@ -634,6 +656,7 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
+    plan->colptr.reset();
     plan->dense.reset();
     plan->dense_ready = false;
     plan->resident = false;
@@ -648,6 +671,7 @@ BBTC_API void bbtc_plan_free(bbtc_plan* plan) {
   if (plan->h_ccu) cudaFreeHost(plan->h_ccu);
   if (plan->h_ccv) cudaFreeHost(plan->h_ccv);
   if (plan->h_rowptr) cudaFreeHost(plan->h_rowptr);
+  if (plan->h_colptr) cudaFreeHost(plan->h_colptr);
   if (plan->h_epochs) cudaFreeHost(plan->h_epochs);
   delete plan;
 }

@@ -164,6 +164,11 @@ struct bbtc_plan {
   uint32_t* h_rowptr = nullptr;
   uint32_t* h_ccu = nullptr;
   uint32_t* h_ccv = nullptr;
+  // Streamed counts ship each column-major block's column ids as column offsets
+  // (|V_j|+1 words per block instead of nnz) and expand them on the device.
+  uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
+  std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
+  bbtc::DevBuf<uint32_t> colptr;      // device staging of the column offsets (streaming)
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;
   // Dense tasks (Alg. 6's dense map over V_k, chosen per task as isDense,
@@ -225,6 +230,10 @@ void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
 // Dense tasks: build the bit rows (once per resident plan) and count items
 // [item_lo, item_hi) of the dense tasks.
 void dense_build(bbtc_ctx* ctx, bbtc_plan* plan);
+// Column offsets of every column-major block (host plan preparation) and their
+// expansion back to per-edge column ids after a streamed copy (copy stream).
+uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, bbtc::DevBuf<uint32_t>* out);
+void colptr_expand(cudaStream_t st, const uint32_t* colptr, uint32_t ncols, uint32_t* ccv);
 void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                         uint64_t item_lo, uint64_t item_hi);
 // capi.cpp (host)

@@ -280,6 +280,45 @@ __global__ void k_row_local(const BlockDesc* __restrict__ blocks, uint32_t nb, c
   }
 }
 
+// ---- a6 support: column offsets of column-major blocks ---------------------------
+// colptr[co[b] + c] = global index of the first edge of column c in block b (runs of
+// ccv), colptr[co[b] + |V_j|] = the block's end; unset entries (empty columns) are
+// filled by a reverse min-scan, then made block-local (k_col_local).
+__global__ void k_col_starts(const uint32_t* __restrict__ ccv, const BlockDesc* __restrict__ blocks,
+                             const uint64_t* __restrict__ co, uint32_t nb, const uint32_t* __restrict__ cuts,
+                             uint32_t* __restrict__ colptr) {
+  for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const BlockDesc B = blocks[b];
+    uint32_t* C = colptr + co[b];
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < B.nnz;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+      const uint32_t c = ccv[B.e0 + x];
+      if (x == 0 || ccv[B.e0 + x - 1] != c) C[c] = (uint32_t)(B.e0 + x);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) C[cuts[B.j + 1] - cuts[B.j]] = (uint32_t)(B.e0 + B.nnz);
+  }
+}
+__global__ void k_col_local(const BlockDesc* __restrict__ blocks, const uint64_t* __restrict__ co, uint32_t nb,
+                            const uint32_t* __restrict__ cuts, uint32_t* __restrict__ colptr) {
+  for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const BlockDesc B = blocks[b];
+    const uint32_t len = cuts[B.j + 1] - cuts[B.j] + 1;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < len; c += gridDim.x * blockDim.x)
+      colptr[co[b] + c] -= (uint32_t)B.e0;
+  }
+}
+// Expansion after a streamed copy: ccv[x] = c for every edge x of column c.  One-warp
+// CTAs with few registers, so they find room next to the persistent count kernel
+// (5 CTAs of 256 threads x <= 48 registers leave 4096 registers per SM) that waits
+// for the ready flag queued behind this kernel.
+__global__ void __launch_bounds__(32) k_col_expand(const uint32_t* __restrict__ colptr, uint32_t ncols,
+                                                   uint32_t* __restrict__ ccv) {
+  for (uint32_t c = blockIdx.x * 32 + threadIdx.x; c < ncols; c += gridDim.x * 32) {
+    const uint32_t x1 = colptr[c + 1];
+    for (uint32_t x = colptr[c]; x < x1; ++x) ccv[x] = c;
+  }
+}
+
 // Transpose keys: (block of edge e) << cb | local column.  Blocks are contiguous edge
 // ranges, found by binary search over their first edges (held in shared memory).
 template <class K>
@@ -784,6 +823,50 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   plan_tasks(plan, 1);
   tr.mark("tasks");
   if (flags & BBTC_PLAN_STATS) plan_stats(ctx, plan);
+}
+
+// Column offsets of every block of a column-major plan (the streamed form of ccv).
+uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t nb = (uint32_t)plan->blocks.size();
+  plan->co_off.assign(nb + 1, 0);
+  uint32_t maxw = 1;
+  for (uint32_t b = 0; b < nb; ++b) {
+    const BlockDesc& B = plan->blocks[b];
+    const uint32_t w = plan->cuts[B.j + 1] - plan->cuts[B.j];
+    maxw = std::max(maxw, w + 1);
+    plan->co_off[b + 1] = plan->co_off[b] + w + 1;
+  }
+  const uint64_t len = plan->co_off[nb];
+  out->alloc(std::max<uint64_t>(len, 1), ctx);
+  DevBuf<uint64_t> dco;
+  DevBuf<uint32_t> dcuts;
+  dco.alloc(nb + 1, ctx);
+  dcuts.alloc(plan->cuts.size(), ctx);
+  BBTC_CUDA(cudaMemcpyAsync(dco.p, plan->co_off.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemcpyAsync(dcuts.p, plan->cuts.data(), plan->cuts.size() * 4, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemsetAsync(out->p, 0xFF, len * 4, st));
+  if (nb) {
+    k_col_starts<<<dim3(64, std::min(nb, 16384u)), kThreads, 0, st>>>(plan->ccv.p, plan->d_blocks.p, dco.p, nb,
+                                                                      dcuts.p, out->p);
+    BBTC_LAUNCHED(ctx);
+    thrust::reverse_iterator<uint32_t*> rin(out->p + len);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::InclusiveScan(t, b, rin, rin, MinOp{}, len, st);
+    });
+    dim3 grid(std::max(1u, std::min((maxw + kThreads - 1) / kThreads, 64u)), std::min(nb, 16384u));
+    k_col_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dco.p, nb, dcuts.p, out->p);
+    BBTC_LAUNCHED(ctx);
+  }
+  BBTC_CUDA(cudaStreamSynchronize(st));   // dco / dcuts die with this scope
+  return len;
+}
+
+void colptr_expand(cudaStream_t st, const uint32_t* colptr, uint32_t ncols, uint32_t* ccv) {
+  if (!ncols) return;
+  const uint32_t grid = std::min<uint32_t>((ncols + 31) / 32, 4096u);
+  k_col_expand<<<grid, 32, 0, st>>>(colptr, ncols, ccv);
+  BBTC_CUDA(cudaGetLastError());
 }
 
 }  // namespace bbtc

@@ -187,6 +187,18 @@ def test_device_input_streaming_and_ranks(ctx, row_major):
     assert plan.info()["host_blocks"] == 1
     tot2, pt2, tm = plan.count(timing=True)
     assert tot2 == otot and np.array_equal(pt2, opt) and tm["h2d_bytes"] > 0
+    # streamed counts take the tasks in unlock order: a rank split still sums to the total
+    acc = np.zeros_like(pt)
+    for r in range(3):
+        plan.unstage()
+        acc += plan.count(rank=r, world=3)[1]
+    assert np.array_equal(acc, opt)
+    # column-major blocks ship their column ids as column offsets (fewer bytes than
+    # the blocks' device form); row-major blocks travel as they are
+    if row_major:
+        assert tm["h2d_bytes"] == plan.info()["block_bytes"]
+    else:
+        assert tm["h2d_bytes"] < plan.info()["block_bytes"]
     tot3, pt3, tm3 = plan.count(timing=True)           # now resident: no copies
     assert tot3 == otot and tm3["h2d_bytes"] == 0
     plan.unstage()
