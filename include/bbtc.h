@@ -165,6 +165,9 @@ typedef struct {
   uint32_t dense_tasks;     /* tasks counted through bit rows over V_k (isDense) */
   uint32_t dense_bits;      /* largest |V_k| a dense task may have (0 = dense path off) */
   uint64_t dense_bytes;     /* device bytes of the bit rows (0 until the first resident count) */
+  uint64_t stream_bytes;    /* host->device bytes that bring every block to the device once
+                               (bbtc_plan_to_host plans: column-major blocks cross PCIe with
+                               column offsets instead of per-edge column ids); else 0 */
 } bbtc_plan_info;
 
 #define BBTC_PLAN_STATS 1u     /* compute b_alg / visits / dmax_blk (one extra device pass) */

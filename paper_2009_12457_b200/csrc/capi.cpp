@@ -298,25 +298,24 @@ struct Streamer {
   }
   // Copies block b from the pinned host arenas to device arenas (edge arrays at
   // edge offset e_dst, row offsets at ro_dst), then its ready flag = epoch.
-  // expand: ship a column-major block's column ids as its column offsets (|V_j|+1
-  // words instead of nnz: 8 instead of 12 bytes per edge) and expand them into the
-  // device ccv on the copy stream, before the ready flag.
+  // expand: a column-major block's column ids cross PCIe as its column offsets
+  // (|V_j|+1 words instead of nnz: 8 instead of 12 bytes per edge), read straight from
+  // the mapped pinned arena by the expansion kernel on the copy stream, which writes
+  // the device ccv before the ready flag.
   void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst,
             bool expand = false) {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
     auto arenas = plan->edge_arenas();
-    expand = expand && plan->colmajor && plan->h_colptr && plan->colptr.p;
+    expand = expand && plan->colmajor && plan->hd_colptr;
     const size_t direct = expand ? 2 : arenas.size();   // arena 2 (ccv) comes from the offsets
     if (B.nnz)
       for (size_t x = 0; x < direct; ++x)
         BBTC_CUDA(cudaMemcpyAsync(dev_edges[x] + e_dst, *arenas[x].host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
     if (expand && B.nnz) {
       const uint32_t ncols = plan->cuts[B.j + 1] - plan->cuts[B.j];
-      BBTC_CUDA(cudaMemcpyAsync(plan->colptr.p + plan->co_off[b], plan->h_colptr + plan->co_off[b],
-                                ((uint64_t)ncols + 1) * 4, cudaMemcpyHostToDevice, cs));
-      colptr_expand(cs, plan->colptr.p + plan->co_off[b], ncols, dev_edges[2] + e_dst);
+      colptr_expand(cs, plan->hd_colptr + plan->co_off[b], ncols, dev_edges[2] + e_dst);
       ctx->launches++;
       bytes += ((uint64_t)ncols + 1) * 4;
     }
@@ -418,7 +417,6 @@ static uint64_t rowptr_len(const bbtc_plan* plan) {
 
 static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
   if (!plan->rowptr.p) plan->rowptr.alloc(rowptr_len(plan), ctx);
-  if (plan->h_colptr && !plan->colptr.p) plan->colptr.alloc(std::max<uint64_t>(plan->co_off.back(), 1), ctx);
   for (auto& A : plan->edge_arenas())
     if (!A.dev->p && plan->m) A.dev->alloc(plan->m, ctx);
 }
@@ -622,9 +620,17 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (plan->colmajor) {   // the streamed form of ccv: per-block column offsets
       DevBuf<uint32_t> cp;
       const uint64_t len = colptr_build(ctx, plan, &cp);
-      BBTC_CUDA(cudaHostAlloc((void**)&plan->h_colptr, std::max<uint64_t>(len, 1) * 4, cudaHostAllocPortable));
+      BBTC_CUDA(cudaHostAlloc((void**)&plan->h_colptr, std::max<uint64_t>(len, 1) * 4,
+                              cudaHostAllocPortable | cudaHostAllocMapped));
+      BBTC_CUDA(cudaHostGetDevicePointer((void**)&plan->hd_colptr, plan->h_colptr, 0));
       BBTC_CUDA(cudaMemcpyAsync(plan->h_colptr, cp.p, len * 4, cudaMemcpyDeviceToHost, st));
       BBTC_CUDA(cudaStreamSynchronize(st));
+    }
+    plan->info.stream_bytes = 0;
+    for (const BlockDesc& B : plan->blocks) {
+      plan->info.stream_bytes += 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+      if (plan->colmajor && B.nnz) plan->info.stream_bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.j + 1] - plan->cuts[B.j]) + 1);
+      else plan->info.stream_bytes += 4 * B.nnz * plan->edge_arenas().size();
     }
     BBTC_CUDA(cudaStreamSynchronize(st));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
@@ -656,7 +662,6 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
-    plan->colptr.reset();
     plan->dense.reset();
     plan->dense_ready = false;
     plan->resident = false;
@@ -1049,7 +1054,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         s.epoch = epoch;
         if (wait_for >= 0)
           for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, ev_done[wait_for], 0));
-        for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b]);
+        for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b], !getenv("BBTC_NO_COLPTR"));
         for (uint32_t b : wblocks)
           if (std::find(load.begin(), load.end(), b) == load.end())
             s.flag(b, ctx->copy_streams[s.rr++ % ctx->copy_streams.size()]);

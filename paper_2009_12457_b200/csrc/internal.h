@@ -165,10 +165,11 @@ struct bbtc_plan {
   uint32_t* h_ccu = nullptr;
   uint32_t* h_ccv = nullptr;
   // Streamed counts ship each column-major block's column ids as column offsets
-  // (|V_j|+1 words per block instead of nnz) and expand them on the device.
+  // (|V_j|+1 words per block instead of nnz), read by the device from this mapped
+  // pinned arena and expanded into ccv.
   uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
+  uint32_t* hd_colptr = nullptr;      // the same arena's device (mapped) address
   std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
-  bbtc::DevBuf<uint32_t> colptr;      // device staging of the column offsets (streaming)
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;
   // Dense tasks (Alg. 6's dense map over V_k, chosen per task as isDense,

@@ -195,10 +195,12 @@ def test_device_input_streaming_and_ranks(ctx, row_major):
     assert np.array_equal(acc, opt)
     # column-major blocks ship their column ids as column offsets (fewer bytes than
     # the blocks' device form); row-major blocks travel as they are
+    info = plan.info()
+    assert tm["h2d_bytes"] == info["stream_bytes"]
     if row_major:
-        assert tm["h2d_bytes"] == plan.info()["block_bytes"]
+        assert info["stream_bytes"] == info["block_bytes"]
     else:
-        assert tm["h2d_bytes"] < plan.info()["block_bytes"]
+        assert info["stream_bytes"] < info["block_bytes"]
     tot3, pt3, tm3 = plan.count(timing=True)           # now resident: no copies
     assert tot3 == otot and tm3["h2d_bytes"] == 0
     plan.unstage()
@@ -252,7 +254,7 @@ def test_out_of_core_budget(ctx, frac, row_major):
     for _ in range(2):   # twice: the second count reuses nothing (cache dies with the call)
         tot, pt, tm = plan.count(timing=True)
         assert tot == otot and np.array_equal(pt, opt)
-        assert tm["h2d_bytes"] >= total_bytes
+        assert tm["h2d_bytes"] >= plan.info()["stream_bytes"] > 0   # every block at least once
     plan.set_budget(1024)   # smaller than any task's blocks
     with pytest.raises(bb.BBTCError):
         plan.count()
