@@ -155,7 +155,8 @@ typedef struct {
   uint32_t dmax_blk;        /* d'_max: largest partial degree d(G_ij,u) over all blocks */
   uint32_t host_blocks;     /* 1 if the blocks live in pinned host memory (bbtc_plan_to_host) */
   uint64_t block_bytes;     /* bytes of all blocks (row offsets + cols + row ids) */
-  uint64_t max_task_bytes;  /* largest 3-block footprint of one task */
+  uint64_t max_task_bytes;  /* largest footprint of one task: device bytes of its distinct
+                               blocks (row offsets + per-edge arrays) */
   uint64_t b_alg;           /* algorithmic bytes of the count, 0 unless
                                BBTC_PLAN_STATS was passed */
   uint64_t visits;          /* edge visits summed over tasks, i.e. sum_t nnz(G_ij); ditto */
@@ -191,6 +192,18 @@ typedef struct {
  * ceil(log2 p) > 64 bits of sort key), BBTC_ENOMEM, BBTC_ECUDA. */
 BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
                                       uint32_t flags, bbtc_plan** out);
+/* a3, automatic p (p is chosen so that "three subgraphs can fit into memory
+ * of the computing devices"): *p = the smallest p (1 … min(n, 256)) such that, under
+ * the default cut rule, the largest task footprint — the device bytes of the task's
+ * distinct blocks (row offsets + per-edge arrays, as bbtc_plan_info.max_task_bytes
+ * counts them for the given flags) — times `depth` (tasks in flight at once; 0 = 1)
+ * is at most budget_bytes.  One pass over the edges per candidate p (candidates 1, 2,
+ * 4, … until one fits, then the smallest fitting p below it); no blocks are built.
+ * Use the result with bbtc_plan_create and, for a budget below the plan's bytes,
+ * bbtc_plan_to_host + bbtc_plan_set_budget.
+ * Errors: BBTC_EINVAL (NULL, budget 0), BBTC_ERANGE (no p <= min(n, 256) fits). */
+BBTC_API bbtc_status bbtc_plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget_bytes, uint32_t depth,
+                                      uint32_t flags, uint32_t* p);
 BBTC_API bbtc_status bbtc_plan_info_get(const bbtc_plan* plan, bbtc_plan_info* info);
 /* cuts: host, p+1 entries. */
 BBTC_API bbtc_status bbtc_plan_cuts(const bbtc_plan* plan, uint32_t* cuts);

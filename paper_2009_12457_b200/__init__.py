@@ -19,7 +19,7 @@ from . import _lib as L
 from ._lib import BBTCError, MEM_DEVICE, MEM_HOST, PLAN_STATS
 
 __all__ = ["Context", "Graph", "Plan", "BBTCError", "n_tasks", "task_index", "task_ijk", "count_triangles",
-           "read_edges", "FORMATS"]
+           "read_edges", "FORMATS", "auto_p"]
 
 FORMATS = {"text": L.FMT_TEXT, "mm": L.FMT_MM, "bin": L.FMT_BIN}
 
@@ -155,6 +155,14 @@ class Graph:
 
     def __del__(self):
         self.close()
+
+
+def auto_p(ctx: "Context", graph: "Graph", budget_bytes: int, depth: int = 2, row_major: bool = False) -> int:
+    """bbtc_plan_auto_p: the smallest p whose largest task footprint x depth fits the budget."""
+    p = ctypes.c_uint32()
+    L.check(L.bbtc_plan_auto_p(ctx.handle, graph._h, int(budget_bytes), depth,
+                               L.PLAN_ROWMAJOR if row_major else 0, ctypes.byref(p)))
+    return int(p.value)
 
 
 class Plan:

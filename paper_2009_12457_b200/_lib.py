@@ -88,6 +88,7 @@ bbtc_edges_read = _sig("bbtc_edges_read", _st, ctypes.c_char_p, ctypes.c_int, ct
 bbtc_edges_free = _sig("bbtc_edges_free", None, ctypes.POINTER(bbtc_edge_list))
 bbtc_graph_load = _sig("bbtc_graph_load", _st, _vp, ctypes.c_char_p, ctypes.c_int, c_u32, _pp)
 bbtc_plan_create = _sig("bbtc_plan_create", _st, _vp, _vp, c_u32, _u32p, c_u32, _pp)
+bbtc_plan_auto_p = _sig("bbtc_plan_auto_p", _st, _vp, _vp, c_u64, c_u32, c_u32, _u32p)
 bbtc_plan_info_get = _sig("bbtc_plan_info_get", _st, _vp, ctypes.POINTER(bbtc_plan_info))
 bbtc_plan_cuts = _sig("bbtc_plan_cuts", _st, _vp, _u32p)
 bbtc_plan_block = _sig("bbtc_plan_block", _st, _vp, _vp, c_u32, c_u32, _u32p, _u32p, _u32p, _u64p)

@@ -163,9 +163,10 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   plan->chunk = 0;
   plan->item_start.assign(1, 0);
   uint64_t max_task_bytes = 0;
+  const uint64_t arenas = plan->colmajor ? 3 : 2;   // per-edge u32 arrays of a block on the device
   auto bbytes = [&](uint32_t b) {
     const BlockDesc& B = plan->blocks[b];
-    return 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+    return 4 * arenas * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
   };
   // Execution order: "kji" (default: k outer, i inner — consecutive tasks share G_jk
   // and walk G_ik) or "ijk" (Alg. 4's own order), BBTC_TASK_ORDER overrides.
@@ -562,6 +563,16 @@ BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32
       throw;
     }
     *out = plan;
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget_bytes, uint32_t depth,
+                                      uint32_t flags, uint32_t* p) {
+  return guard([&] {
+    if (!ctx || !g || !p) raise(BBTC_EINVAL, "NULL argument");
+    if (budget_bytes == 0) raise(BBTC_EINVAL, "budget must be > 0");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    *p = plan_auto_p(ctx, g, budget_bytes, depth, flags);
   });
 }
 

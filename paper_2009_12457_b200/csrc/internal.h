@@ -102,6 +102,7 @@ constexpr int kCursorSlots = 1024;
 constexpr uint32_t kDenseMinS = 8;     // bit-row strides (words): powers of two in [8, 256]
 constexpr uint32_t kDenseMaxS = 256;
 constexpr uint32_t kDenseBitsDefault = 2048;
+constexpr uint32_t kAutoPMax = 256;   // largest p the automatic choice tries
 
 struct bbtc_graph {
   bbtc_ctx* ctx = nullptr;
@@ -228,6 +229,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
                   const DevArenas* arenas = nullptr, const TaskDesc* tasks = nullptr,
                   const uint64_t* item_start = nullptr);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
+uint32_t plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget, uint32_t depth, uint32_t flags);
 // Dense tasks: build the bit rows (once per resident plan) and count items
 // [item_lo, item_hi) of the dense tasks.
 void dense_build(bbtc_ctx* ctx, bbtc_plan* plan);

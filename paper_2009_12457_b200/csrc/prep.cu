@@ -280,6 +280,30 @@ __global__ void k_row_local(const BlockDesc* __restrict__ blocks, uint32_t nb, c
   }
 }
 
+// ---- a3 auto-p: block sizes of a candidate partition without building it ---------
+// hist[i*p + j] = edges (ru, rw) with ru in V_i, rw in V_j (the nnz of block (i,j)).
+__global__ void k_part_hist(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
+                            uint32_t p, bool smem_hist, unsigned long long* __restrict__ hist) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* s_cuts = sh;
+  uint32_t* s_hist = sh + p + 1;
+  for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+  if (smem_hist)
+    for (uint32_t x = threadIdx.x; x < p * p; x += blockDim.x) s_hist[x] = 0;
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = okeys[e];
+    const uint32_t i = part_of(s_cuts, p, (uint32_t)(k >> 32)), j = part_of(s_cuts, p, (uint32_t)k);
+    if (smem_hist) atomicAdd(&s_hist[i * p + j], 1u);
+    else atomicAdd(&hist[i * p + j], 1ull);
+  }
+  if (smem_hist) {
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < p * p; x += blockDim.x)
+      if (s_hist[x]) atomicAdd(&hist[x], (unsigned long long)s_hist[x]);
+  }
+}
+
 // ---- a6 support: column offsets of column-major blocks ---------------------------
 // colptr[co[b] + c] = global index of the first edge of column c in block b (runs of
 // ccv), colptr[co[b] + |V_j|] = the block's end; unset entries (empty columns) are
@@ -867,6 +891,74 @@ void colptr_expand(cudaStream_t st, const uint32_t* colptr, uint32_t ncols, uint
   const uint32_t grid = std::min<uint32_t>((ncols + 31) / 32, 4096u);
   k_col_expand<<<grid, 32, 0, st>>>(colptr, ncols, ccv);
   BBTC_CUDA(cudaGetLastError());
+}
+
+// a3, automatic p: the smallest p whose largest task
+// footprint (the device bytes of its distinct blocks: row offsets + per-edge arrays)
+// times `depth` (tasks whose blocks are in flight at once) fits `budget`.  Each
+// candidate costs one pass over the oriented edges (default cuts + a block histogram,
+// no BCSR).  Candidates 1, 2, 4, … until one fits, then the smallest fitting p below it.
+uint32_t plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget, uint32_t depth, uint32_t flags) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  const uint64_t arenas = (flags & BBTC_PLAN_ROWMAJOR) ? 2 : 3;
+  depth = std::max(depth, 1u);
+  const uint32_t pmax = std::max(1u, std::min<uint32_t>(n, kAutoPMax));
+  DevBuf<uint64_t> incl;
+  if (n > 0) {
+    incl.alloc(n, ctx);
+    cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(g->deg_sorted.p, ToU64{});
+    cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, it, incl.p, (uint64_t)n, st); });
+  }
+  DevBuf<uint32_t> dc;
+  dc.alloc(pmax + 1, ctx);
+  DevBuf<unsigned long long> hist;
+  hist.alloc((uint64_t)pmax * pmax, ctx);
+  auto footprint = [&](uint32_t p) -> uint64_t {
+    std::vector<uint32_t> cuts(p + 1, 0);
+    cuts[p] = n;
+    if (n > 0 && p > 1) {
+      k_cuts<<<1, 256, 0, st>>>(incl.p, n, 2 * m, p, dc.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaMemcpyAsync(cuts.data(), dc.p, (p + 1) * 4, cudaMemcpyDeviceToHost, st));
+    } else {
+      BBTC_CUDA(cudaMemcpyAsync(dc.p, cuts.data(), (p + 1) * 4, cudaMemcpyHostToDevice, st));
+    }
+    BBTC_CUDA(cudaMemsetAsync(hist.p, 0, (uint64_t)p * p * 8, st));
+    if (m) {
+      const bool sm = p <= 64;
+      const size_t smem = (p + 1) * 4 + (sm ? (size_t)p * p * 4 : 0);
+      k_part_hist<<<grid_for(ctx, m), kThreads, smem, st>>>(g->okeys.p, m, dc.p, p, sm, hist.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    std::vector<unsigned long long> h((uint64_t)p * p);
+    BBTC_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    auto bytes = [&](uint32_t i, uint32_t j) {
+      return 4 * arenas * (uint64_t)h[(uint64_t)i * p + j] + 4 * ((uint64_t)(cuts[i + 1] - cuts[i]) + 1);
+    };
+    uint64_t worst = 0;
+    for (uint32_t i = 0; i < p; ++i)
+      for (uint32_t j = i; j < p; ++j)
+        for (uint32_t k = j; k < p; ++k) {
+          // distinct blocks: ik == ij iff j == k; jk == ik iff i == j
+          const uint64_t t = bytes(i, j) + (k != j ? bytes(i, k) : 0) + (i != j ? bytes(j, k) : 0);
+          worst = std::max(worst, t);
+        }
+    return worst;
+  };
+  auto fits = [&](uint32_t p) { return footprint(p) <= budget / depth; };
+  uint32_t hi = 1;
+  while (!fits(hi)) {
+    if (hi >= pmax)
+      raise(BBTC_ERANGE, "device budget " + std::to_string(budget) + " B is below the largest task footprint at p = " +
+                             std::to_string(pmax) + " (x depth " + std::to_string(depth) + ")");
+    hi = std::min(2 * hi, pmax);
+  }
+  for (uint32_t p = hi / 2 + 1; p < hi; ++p)
+    if (fits(p)) return p;
+  return hi;
 }
 
 }  // namespace bbtc

@@ -360,3 +360,30 @@ def test_dense_strides(gpu):
     assert int(tot) == otot
     assert [int(x) for x in pts.split(",")] == [int(x) for x in opt]
     assert int(nd) > 60   # of 165 tasks: every one with k >= 1 and a non-empty G_ij
+
+
+def test_auto_p_from_budget(ctx):
+    """bbtc_plan_auto_p: the smallest p whose largest task fits the budget."""
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(16, 16, 5)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 16)
+    whole = bb.Plan(ctx, g, 1).info()["max_task_bytes"]
+    assert bb.auto_p(ctx, g, whole, depth=1) == 1
+    for frac, depth in ((0.4, 1), (0.4, 2), (0.15, 1)):
+        budget = int(whole * frac)
+        p = bb.auto_p(ctx, g, budget, depth=depth)
+        assert p > 1
+        assert bb.Plan(ctx, g, p).info()["max_task_bytes"] * depth <= budget
+        for q in range(1, p):   # smallest such p
+            assert bb.Plan(ctx, g, q).info()["max_task_bytes"] * depth > budget
+    p = bb.auto_p(ctx, g, int(whole * 0.4), depth=1)
+    plan = bb.Plan(ctx, g, p)
+    otot, opt, _, _ = og.count(p)
+    plan.to_host()
+    plan.set_budget(int(whole * 0.4) * 3)   # a few tasks' blocks at a time
+    tot, pt = plan.count()
+    assert tot == otot and np.array_equal(pt, opt)
+    with pytest.raises(bb.BBTCError) as ei:
+        bb.auto_p(ctx, g, 1000)
+    assert ei.value.code == -5
