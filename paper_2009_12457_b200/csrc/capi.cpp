@@ -240,6 +240,12 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         T.idx = (uint32_t)task_index(p, i, j, k);
         if (plan->tasks.size() == plan->dense_task_lo) plan->dense_item_lo = plan->item_start.back();
         T.pad = plan->tasks.size() >= plan->dense_task_lo ? plan->dense_s[k] : 0;
+        {
+          const uint32_t vk = plan->cuts[k + 1] - plan->cuts[k];
+          uint32_t w = 4;
+          while (w * 32 < vk) w <<= 1;
+          T.bmw = (vk > 0 && w <= kBitmapMaxWords) ? w : 0;
+        }
         // A list edge costs its lists; a dense edge a fixed number of bit-row words.
         // Dense tasks take the smaller of both chunks: without resident blocks (streamed,
         // out of core) the list kernel runs them too.

@@ -36,6 +36,11 @@ constexpr int kMinCtas = BBTC_MIN_CTAS;   // register budget: >= 5 CTAs (40 warp
 #define BBTC_PREFETCH 1
 #endif
 constexpr bool kPrefetch = BBTC_PREFETCH;   // L2 prefetch of a batch's probe lists
+#ifndef BBTC_BITMAP
+#define BBTC_BITMAP 1
+#endif
+constexpr bool kBitmap = BBTC_BITMAP;   // single-list batches over a small V_k use a bitmap
+static_assert(kBitmapMaxWords == (uint32_t)kTable, "a bitmap over V_k must fit the per-warp table");
 constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -59,7 +64,7 @@ __device__ __forceinline__ uint32_t hbucket(uint32_t key, int shift) { return (k
 // the current window plus a popc.  `load(f, P)` fetches the position's word two
 // windows ahead of `use(f, P, w)` (software pipelining of the gather).
 template <class Ld, class Use>
-__device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uint32_t start, uint4 payload,
+__device__ __forceinline__ void flatten(uint2* pay, int lane, bool nonempty, uint32_t start, uint2 payload,
                                         uint32_t total, Ld load, Use use) {
   const uint32_t nmask = __ballot_sync(kFull, nonempty);
   if (nonempty) pay[__popc(nmask & lanemask_lt(lane))] = payload;
@@ -73,14 +78,14 @@ __device__ __forceinline__ void flatten(uint4* pay, int lane, bool nonempty, uin
     before += __popc(starts);
     return idx;
   };
-  uint4 P0 = pay[owner(0)], P1 = P0;
+  uint2 P0 = pay[owner(0)], P1 = P0;
   uint32_t w0 = lane < total ? load(lane, P0) : 0, w1 = 0;
   if (32 < total) {
     P1 = pay[owner(32)];
     if (32 + lane < total) w1 = load(32 + lane, P1);
   }
   for (uint32_t f0 = 0; f0 < total; f0 += 32) {
-    uint4 P2 = P1;
+    uint2 P2 = P1;
     uint32_t w2 = 0;
     const uint32_t f2 = f0 + 64 + lane;
     if (f0 + 64 < total) {
@@ -122,11 +127,10 @@ __device__ __forceinline__ uint32_t table_probe(const uint4* tab4, uint32_t hk, 
 // Probe lists of lanes: P = cols[bx .. bx + bl).  Phase 1 walks the long lists one at
 // a time in whole 32-word rounds (all lanes on consecutive words of one list, four
 // loads in flight); phase 2 flattens the < 32-word remainders across the lanes.
-// key(w, slot) gives the table key of a probe word.
-template <class Key>
-__device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ cols, const uint4* tab4, uint4* pay,
-                                                int lane, uint32_t bx, uint32_t bl, uint32_t slot, int shift,
-                                                uint32_t bmask, Key key) {
+// test(w, slot) = 1 if probe word w of a lane whose staged list has slot `slot` is in it.
+template <class Test>
+__device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ cols, uint2* pay, int lane, uint32_t bx,
+                                                uint32_t bl, uint32_t slot, Test test) {
   uint32_t hits = 0;
   uint32_t longs = __ballot_sync(kFull, bl >= 32);
   while (longs) {
@@ -138,18 +142,17 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
     uint32_t off = 0;
     for (; off + 128 <= nfull; off += 128) {
       const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
-      hits += table_probe(tab4, key(w1, sl), shift, bmask) + table_probe(tab4, key(w2, sl), shift, bmask) +
-              table_probe(tab4, key(w3, sl), shift, bmask) + table_probe(tab4, key(w4, sl), shift, bmask);
+      hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
     }
-    for (; off < nfull; off += 32) hits += table_probe(tab4, key(B[off], sl), shift, bmask);
+    for (; off < nfull; off += 32) hits += test(B[off], sl);
   }
   const uint32_t rem = bl & 31u;
   const uint32_t rinc = warp_incl_scan(rem, lane);
   const uint32_t total_r = __shfl_sync(kFull, rinc, 31);
   const uint32_t rstart = rinc - rem;
-  flatten(pay, lane, rem > 0, rstart, make_uint4(bx + (bl & ~31u) - rstart, slot, 0, 0), total_r,
-          [&](uint32_t f, uint4 P) { return cols[P.x + f]; },
-          [&](uint32_t, uint4 P, uint32_t w) { hits += table_probe(tab4, key(w, P.y), shift, bmask); });
+  flatten(pay, lane, rem > 0, rstart, make_uint2(bx + (bl & ~31u) - rstart, slot), total_r,
+          [&](uint32_t f, uint2 P) { return cols[P.x + f]; },
+          [&](uint32_t, uint2 P, uint32_t w) { hits += test(w, P.y); });
   return hits;
 }
 
@@ -160,7 +163,7 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
 // is probed once per chunk.  Returns this lane's hits.
 __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ cS,
                                            uint32_t s0, uint32_t total_a, uint32_t bx, uint32_t bl, uint32_t* tab,
-                                           uint4* pay, int lane) {
+                                           uint2* pay, int lane) {
   uint4* tab4 = reinterpret_cast<uint4*>(tab);
   uint32_t hits = 0;
   for (uint32_t c0 = 0; c0 < total_a; c0 += kChunk) {
@@ -173,7 +176,8 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
     __syncwarp();
     for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, cS[s0 + c0 + x], shift, bmask);
     __syncwarp();
-    hits += probe_lists(cols, tab4, pay, lane, bx, bl, 0, shift, bmask, [](uint32_t w, uint32_t) { return w; });
+    hits += probe_lists(cols, pay, lane, bx, bl, 0,
+                        [&](uint32_t w, uint32_t) { return table_probe(tab4, w, shift, bmask); });
   }
   return hits;
 }
@@ -182,7 +186,7 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
 // with slot-tagged keys (w << 5 | slot), which needs |V_k| < 2^27; otherwise every
 // batch takes one staged list at a time (long_list).  kCol: walk G_ij by column
 // (ccu/ccv arrays, stage N(G_jk,v)) or by row (rows/cols, stage N(G_ik,u)).
-template <bool kSlots, bool kCol>
+template <bool kSlots, bool kCol, bool kBm>
 __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
         const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
@@ -194,7 +198,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
   const int wid = threadIdx.x >> 5;
   uint32_t* tab = smem + wid * kTable;
   uint4* tab4 = reinterpret_cast<uint4*>(tab);
-  uint4* pay = reinterpret_cast<uint4*>(smem + kWarps * kTable) + wid * 32;
+  uint2* pay = reinterpret_cast<uint2*>(smem + kWarps * kTable) + wid * 32;
 
   for (;;) {
     unsigned long long it = 0;
@@ -263,8 +267,13 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const uint32_t incl = warp_incl_scan(lead_len, lane);
       const uint32_t aoff = __shfl_sync(kFull, incl - lead_len, my_leader);
       const uint32_t aend = aoff + alen;
+      // Small V_k and few distinct staged lists in the batch (all of them fit the table
+      // as bitmaps over V_k, T.bmw words each): bitmaps instead of a hash table (one
+      // LDS + a bit test per probe word, any list length).
+      const bool bm_path = kBm && T.bmw != 0 && __popc(lmask) * T.bmw <= (uint32_t)kTable;
       // lanes [0,L) whose staged lists fit one shared table (load <= 1/4)
-      int L = kSlots ? __popc(__ballot_sync(kFull, valid && aend <= kHashCap)) : 0;
+      int L = bm_path ? __popc(__ballot_sync(kFull, valid))
+                      : kSlots ? __popc(__ballot_sync(kFull, valid && aend <= kHashCap)) : 0;
       bool dense = false;   // one list of kHashCap..kChunk words: a table of its own, load <= 1/2
       bool longl = false;   // longer (or untaggable): the out-of-line chunked path
       if (L == 0) {
@@ -286,8 +295,52 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         const uint32_t lines = min((bl + 31) >> 5, 4u);
         for (uint32_t x = 0; x < lines; ++x) asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + 32 * x));
       }
+      // A staged list that fills the whole batch usually continues (a column with many
+      // edges): keep its table and probe the run's next edges against it, instead of
+      // re-reading and re-hashing the list for every 32 edges.
+      auto continue_run = [&](auto test) {
+        const uint32_t k0 = __shfl_sync(kFull, key, 0);
+        if (L == 32 && __all_sync(kFull, valid && key == k0)) {
+          for (;;) {
+            const uint64_t e2 = base + L + lane;
+            const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
+            const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
+            if (L2 == 0) break;
+            uint32_t b2 = 0, bl2 = 0;
+            if (ok && alen > 0) {
+              const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
+              b2 = rpP[p2];
+              bl2 = rpP[p2 + 1] - b2;
+            }
+            hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
+            L += L2;
+            if (L2 < 32) break;
+          }
+        }
+      };
       if (__any_sync(kFull, bl > 0)) {
-        if (longl) {
+        if (bm_path) {
+          uint32_t* bm = tab;
+          const uint32_t bmw = T.bmw;
+          const uint32_t words = __popc(lmask) * bmw;
+          for (uint32_t x = 4 * lane; x < words; x += 128) *reinterpret_cast<uint4*>(bm + x) = make_uint4(0, 0, 0, 0);
+          __syncwarp();
+          if (lmask == 1u) {   // one list: coalesced reads, no flattening
+            const uint32_t s0 = __shfl_sync(kFull, a0, 0), sn = __shfl_sync(kFull, alen, 0);
+            for (uint32_t x = lane; x < sn; x += 32) {
+              const uint32_t w = cS[s0 + x];
+              atomicOr(bm + (w >> 5), 1u << (w & 31));
+            }
+          } else {
+            flatten(pay, lane, leader && alen > 0, aoff, make_uint2(a0 - aoff, slot * bmw),
+                    __shfl_sync(kFull, aend, L - 1), [&](uint32_t f, uint2 P) { return cS[P.x + f]; },
+                    [&](uint32_t, uint2 P, uint32_t w) { atomicOr(bm + P.y + (w >> 5), 1u << (w & 31)); });
+          }
+          __syncwarp();
+          auto test = [bm](uint32_t w, uint32_t base_w) { return (bm[base_w + (w >> 5)] >> (w & 31)) & 1u; };
+          hits += probe_lists(cols, pay, lane, bx, bl, slot * bmw, test);
+          continue_run(test);
+        } else if (longl) {
           hits += long_list(cols, cS, __shfl_sync(kFull, a0, 0), __shfl_sync(kFull, alen, 0), bx, bl, tab, pay,
                             lane);
         } else {
@@ -299,33 +352,13 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           const int shift = 32 - (__ffs(nb) - 1);
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
-          flatten(pay, lane, in && leader && alen > 0, aoff, make_uint4(a0, aoff, slot, 0), total_a,
-                  [&](uint32_t f, uint4 P) { return cS[P.x + (f - P.y)]; },
-                  [&](uint32_t, uint4 P, uint32_t w) { table_insert(tab, (w << 5) | P.z, shift, bmask); });
+          flatten(pay, lane, in && leader && alen > 0, aoff, make_uint2(a0 - aoff, slot), total_a,
+                  [&](uint32_t f, uint2 P) { return cS[P.x + f]; },
+                  [&](uint32_t, uint2 P, uint32_t w) { table_insert(tab, (w << 5) | P.y, shift, bmask); });
           // ---- probe every word of each lane's list P against its staged list
-          auto tagged = [](uint32_t w, uint32_t sl) { return (w << 5) | sl; };
-          hits += probe_lists(cols, tab4, pay, lane, bx, bl, slot, shift, bmask, tagged);
-          // ---- a staged list that fills the whole batch usually continues (a column
-          // with many edges): keep its table and probe the run's next edges against
-          // it, instead of re-reading and re-hashing the list for every 32 edges.
-          const uint32_t k0 = __shfl_sync(kFull, key, 0);
-          if (L == 32 && __all_sync(kFull, valid && key == k0)) {
-            for (;;) {
-              const uint64_t e2 = base + L + lane;
-              const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
-              const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
-              if (L2 == 0) break;
-              uint32_t b2 = 0, bl2 = 0;
-              if (ok && alen > 0) {
-                const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
-                b2 = rpP[p2];
-                bl2 = rpP[p2 + 1] - b2;
-              }
-              hits += probe_lists(cols, tab4, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, shift, bmask, tagged);
-              L += L2;
-              if (L2 < 32) break;
-            }
-          }
+          auto test = [&](uint32_t w, uint32_t sl) { return table_probe(tab4, (w << 5) | sl, shift, bmask); };
+          hits += probe_lists(cols, pay, lane, bx, bl, slot, test);
+          continue_run(test);
         }
       }
       base += L;
@@ -534,11 +567,17 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
                          const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
                          unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t);
-  const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0);
-  static const KernT kerns[4] = {k_count<false, false>, k_count<true, false>, k_count<false, true>,
-                                 k_count<true, true>};
+  // The bitmap variant only where some task's V_k is small enough (it costs the main
+  // loop a few registers: friendster, whose parts are all large, measured 0.7% slower).
+  bool bm = false;
+  for (const TaskDesc& T : plan->tasks) bm = bm || T.bmw != 0;
+  const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0) | (kBitmap && bm ? 4 : 0);
+  static const KernT kerns[8] = {k_count<false, false, false>, k_count<true, false, false>,
+                                 k_count<false, true, false>,  k_count<true, true, false>,
+                                 k_count<false, false, true>,  k_count<true, false, true>,
+                                 k_count<false, true, true>,   k_count<true, true, true>};
   KernT kern = kerns[variant];
-  static int per_sm[4] = {0, 0, 0, 0};
+  static int per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (!per_sm[variant]) {
     BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     // Shared-memory carveout: what the resident CTAs need, the rest stays L1 for the

@@ -102,7 +102,8 @@ constexpr int kCursorSlots = 1024;
 constexpr uint32_t kDenseMinS = 8;     // bit-row strides (words): powers of two in [8, 256]
 constexpr uint32_t kDenseMaxS = 256;
 constexpr uint32_t kDenseBitsDefault = 2048;
-constexpr uint32_t kAutoPMax = 256;   // largest p the automatic choice tries
+constexpr uint32_t kAutoPMax = 256;
+constexpr uint32_t kBitmapMaxWords = 1024;   // = the count kernel's per-warp table (kTable)   // largest p the automatic choice tries
 
 struct bbtc_graph {
   bbtc_ctx* ctx = nullptr;
@@ -130,7 +131,8 @@ struct TaskDesc {
   uint32_t ij, ik, jk;  // block ids
   uint32_t idx;         // canonical Alg. 4 index
   uint32_t chunk;       // edges of G_ij per work item
-  uint32_t pad;
+  uint32_t pad;         // dense tasks: bit-row stride of V_k in words
+  uint32_t bmw;         // words of a bitmap over V_k (power of two >= 4) if it fits a warp's table, else 0
 };
 
 struct bbtc_plan {

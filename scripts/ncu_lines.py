@@ -1,10 +1,12 @@
 """Per-CUDA-line totals of an ncu SASS source page: stall samples and executed
 instructions, mapped through nvdisasm line info of the same cubin.
 
-    python scripts/ncu_lines.py report.ncu-rep kernel.cubin <mangled-substring> [top]
+    python scripts/ncu_lines.py report.ncu-rep kernel.cubin <mangled-substring> [top] [source.cu]
+    NCU_LINES_INLINE=1: key lines by "line@call-site line" (nvdisasm -gi)
 """
 import csv
 import io
+import os
 import re
 import subprocess
 import sys
@@ -12,7 +14,9 @@ from collections import defaultdict
 
 rep, cubin, fsub = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+INLINE = bool(os.environ.get("NCU_LINES_INLINE"))
+SRC_NAME = os.path.basename(sys.argv[5]) if len(sys.argv) > 5 else ".cu"
+dis = subprocess.run(["nvdisasm", "-gi" if INLINE else "-g", "-c", cubin], capture_output=True, text=True).stdout
 line_of = {}
 cur = None
 infn = False
@@ -25,6 +29,10 @@ for ln in dis.splitlines():
     m = re.search(r'line (\d+)', ln)
     if "//##" in ln and m:
         cur = int(m.group(1))
+        # with -gi: "line N inlined at "<file>", line M" -> key "N@M" (call site in this file)
+        mi = re.search(r'line (\d+) inlined at "([^"]+)", line (\d+)', ln)
+        if mi and INLINE:
+            cur = f"{mi.group(1)}@{mi.group(3)}" if mi.group(2).endswith(SRC_NAME) else f"{mi.group(1)}@ext"
         continue
     m = re.search(r"/\*([0-9a-f]{4,})\*/", ln)
     if m and cur is not None:
@@ -49,5 +57,6 @@ for r in data:
 src = open(sys.argv[5]).read().splitlines() if len(sys.argv) > 5 else None
 print(f"mapped {len(line_of)} SASS offsets; total samples {tot_s}, warp instructions {tot_i}")
 for L, (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-    txt = src[L - 1].strip()[:90] if src and 0 < L <= len(src) else ""
-    print(f"{L:5d} {100 * s / tot_s:6.2f}% samp {100 * i / max(tot_i, 1):6.2f}% inst  {txt}")
+    ln = int(str(L).split("@")[0])
+    txt = src[ln - 1].strip()[:80] if src and 0 < ln <= len(src) else ""
+    print(f"{str(L):>9} {100 * s / tot_s:6.2f}% samp {100 * i / max(tot_i, 1):6.2f}% inst  {txt}")
