@@ -40,9 +40,11 @@ for ln in dis.splitlines():
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
+# one section per profiled kernel ("Kernel Name" row, header row, SASS rows): the first
+sec_end = next((x for x in range(2, len(rows)) if rows[x] and rows[x][0] == "Kernel Name"), len(rows))
 h = rows[1]
 ia, iss, iex = h.index("Address"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-data = [r for r in rows[2:] if len(r) == len(h)]
+data = [r for r in rows[2:sec_end] if len(r) == len(h)]
 base = min(int(r[ia], 16) for r in data)
 agg = defaultdict(lambda: [0, 0])
 tot_s = tot_i = 0
