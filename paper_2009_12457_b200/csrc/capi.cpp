@@ -158,8 +158,17 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
       for (uint32_t i = 0; i <= j; ++i)
         work_total += (double)plan->blocks[block_id(i, j)].nnz *
                       (8.0 + delta(block_id(i, k)) + delta(block_id(j, k)));
-  // ~24 items per warp slot of a full B200 (148 SMs x 40 warps).
-  const double item_work = std::max(1.0, work_total / (148.0 * 40 * 24));
+  // ~384 items per warp slot of a full B200 (148 SMs x 40 warps); BBTC_ITEMS_PER_SLOT
+  // overrides.  The estimate is uniform over a task's edges while the real cost is not
+  // (hub columns: long runs x long probe lists), so fine items balance the tail:
+  // rmat24 count 83.0 / 69.5 / 64.5 / 61.8 / 61.0 / 62.0 ms at 24 / 96 / 192 / 384 /
+  // 768 / 1536 per slot; orkut 15.7 / 14.1 / 14.1 / 14.5 / 14.8 / 15.2; friendster flat
+  // (profiles/r01c/ab_items_per_slot*.jsonl).
+  static const double per_slot = [] {
+    const char* e = getenv("BBTC_ITEMS_PER_SLOT");
+    return e ? std::max(1.0, atof(e)) : 384.0;
+  }();
+  const double item_work = std::max(1.0, work_total / (148.0 * 40 * per_slot));
   plan->chunk = 0;
   plan->item_start.assign(1, 0);
   uint64_t max_task_bytes = 0;
