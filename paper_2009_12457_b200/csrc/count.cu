@@ -45,6 +45,9 @@ static_assert(kBitmapMaxWords == (uint32_t)kTable, "a bitmap over V_k must fit t
 #define BBTC_RUN_PIPE 1
 #endif
 constexpr bool kRunPipe = BBTC_RUN_PIPE;   // pipelined column runs (hash-only variant)
+#ifndef BBTC_RUN_PIPE_BM
+#define BBTC_RUN_PIPE_BM 0
+#endif
 constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -305,7 +308,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       auto continue_run = [&](auto test) {
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         if (L == 32 && __all_sync(kFull, valid && key == k0)) {
-          if constexpr (kRunPipe && !kBm) {
+          if constexpr (kRunPipe && (!kBm || BBTC_RUN_PIPE_BM)) {
           // Two-stage pipeline over the run's batches: while batch t is probed, the row
           // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
           // ids of batch t+2 are in flight.  Only in the hash-only variant: measured
