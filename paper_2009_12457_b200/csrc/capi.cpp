@@ -217,7 +217,9 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   plan->dense.reset();
   static const double dense_ratio = [] {
     const char* e = getenv("BBTC_DENSE_RATIO");
-    return e ? atof(e) : 1.0;   // scripts/dense_sweep.py: 0.5-2 equally fast on rmat24, 8x fewer bit-row bytes than 0
+    // measured with 384 items per slot (profiles/r01c/ab_dense_ratio.jsonl): rmat24 count
+    // 61.7 / 60.9 / 58.8 / 58.7 / 59.9 / 65.2 ms at ratio 1 / 2 / 4 / 8 / 16 / 32
+    return e ? atof(e) : 4.0;
   }();
   if (plan->dense_bits && h == 0)
     for (uint32_t k = 0; k < p; ++k) {

@@ -33,7 +33,7 @@ constexpr int kCtasPerSm = 8;        // cap on resident CTAs per SM (BBTC_CTAS_P
 #endif
 constexpr int kMinCtas = BBTC_MIN_CTAS;   // register budget: >= 5 CTAs (40 warps) resident per SM
 #ifndef BBTC_PREFETCH
-#define BBTC_PREFETCH 1
+#define BBTC_PREFETCH 0
 #endif
 constexpr bool kPrefetch = BBTC_PREFETCH;   // L2 prefetch of a batch's probe lists
 #ifndef BBTC_BITMAP
