@@ -337,11 +337,18 @@ struct Streamer {
       ctx->launches++;
       bytes += ((uint64_t)ncols + 1) * 4;
     }
-    BBTC_CUDA(cudaMemcpyAsync(dev_rowptr + ro_dst, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
+    // Row offsets: the block's leading run of zeros (rows before its first non-empty
+    // row — at least the isolated vertices, which hold the lowest ranks) is set on the
+    // device instead of crossing PCIe.
+    const uint64_t z = plan->rp_zero.empty() ? 0 : std::min<uint64_t>(plan->rp_zero[b], rlen);
+    if (z) BBTC_CUDA(cudaMemsetAsync(dev_rowptr + ro_dst, 0, z * 4, cs));
+    if (rlen > z)
+      BBTC_CUDA(cudaMemcpyAsync(dev_rowptr + ro_dst + z, plan->h_rowptr + B.ro + z, (rlen - z) * 4,
+                                cudaMemcpyHostToDevice, cs));
     flag(b, cs);
     if (!ev[b]) BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     BBTC_CUDA(cudaEventRecord(ev[b], cs));
-    bytes += block_bytes(b) - (direct < arenas.size() ? 4 * B.nnz : 0);
+    bytes += block_bytes(b) - (direct < arenas.size() ? 4 * B.nnz : 0) - 4 * z;
   }
   // The ready flag is a 4-byte copy from a read-only pinned table (h_epochs[e] = e)
   // queued behind the block's copies: the copy engine writes it after the data.
@@ -654,9 +661,19 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
       BBTC_CUDA(cudaMemcpyAsync(plan->h_colptr, cp.p, len * 4, cudaMemcpyDeviceToHost, st));
       BBTC_CUDA(cudaStreamSynchronize(st));
     }
+    // leading zero run of every block's row offsets (set on the device when streamed)
+    BBTC_CUDA(cudaStreamSynchronize(st));   // h_rowptr has landed
+    plan->rp_zero.assign(plan->blocks.size(), 0);
+    for (size_t b = 0; b < plan->blocks.size(); ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      const uint32_t* r = plan->h_rowptr + B.ro;
+      const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+      plan->rp_zero[b] = (uint64_t)(std::find_if(r, r + rlen, [](uint32_t x) { return x != 0; }) - r);
+    }
     plan->info.stream_bytes = 0;
-    for (const BlockDesc& B : plan->blocks) {
-      plan->info.stream_bytes += 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+    for (size_t b = 0; b < plan->blocks.size(); ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      plan->info.stream_bytes += 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1 - plan->rp_zero[b]);
       if (plan->colmajor && B.nnz) plan->info.stream_bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.j + 1] - plan->cuts[B.j]) + 1);
       else plan->info.stream_bytes += 4 * B.nnz * plan->edge_arenas().size();
     }

@@ -172,6 +172,7 @@ struct bbtc_plan {
   // pinned arena and expanded into ccv.
   uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
   uint32_t* hd_colptr = nullptr;      // the same arena's device (mapped) address
+  std::vector<uint64_t> rp_zero;      // per block: leading zero entries of its row offsets
   std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;

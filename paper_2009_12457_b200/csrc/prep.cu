@@ -280,6 +280,57 @@ __global__ void k_row_local(const BlockDesc* __restrict__ blocks, uint32_t nb, c
   }
 }
 
+// Packed transpose keys: block b's columns occupy [cbase[b], cbase[b] + |V_j| - trim_j)
+// of one key range, trim_j = the isolated vertices at the start of part j (they have
+// no edges, so no column id below it).  The whole range usually needs fewer bits than
+// (block << column bits) | column: one radix pass fewer (rmat24: 24 bits instead of 32).
+// Shared memory: e0[nb] (u64), cbase[nb] (u32), trim[p] (u32).
+__device__ __forceinline__ uint32_t block_of_edge(const uint64_t* s_e0, uint32_t nb, uint64_t e) {
+  uint32_t lo = 0, hi = nb - 1;   // last block with e0 <= e
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (s_e0[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__global__ void k_transpose_keys_packed(const uint32_t* __restrict__ cols, uint64_t m,
+                                        const BlockDesc* __restrict__ blocks, uint32_t nb,
+                                        const uint32_t* __restrict__ cbase, const uint32_t* __restrict__ trim,
+                                        uint32_t p, uint32_t* __restrict__ keys) {
+  extern __shared__ uint64_t s_pk[];
+  uint64_t* s_e0 = s_pk;
+  uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_pk + nb);
+  uint32_t* s_bt = s_cb + nb;   // per block: trim of its column part
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    s_e0[b] = blocks[b].e0;
+    s_cb[b] = cbase[b];
+    s_bt[b] = trim[blocks[b].j];
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = block_of_edge(s_e0, nb, e);
+    keys[e] = s_cb[b] + cols[e] - s_bt[b];
+  }
+}
+// Sorted packed keys (still in block order) back to local column ids.
+__global__ void k_unpack_cols(uint32_t* __restrict__ ccv, uint64_t m, const BlockDesc* __restrict__ blocks,
+                              uint32_t nb, const uint32_t* __restrict__ cbase, const uint32_t* __restrict__ trim) {
+  extern __shared__ uint64_t s_pk[];
+  uint64_t* s_e0 = s_pk;
+  uint32_t* s_cb = reinterpret_cast<uint32_t*>(s_pk + nb);
+  uint32_t* s_bt = s_cb + nb;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    s_e0[b] = blocks[b].e0;
+    s_cb[b] = cbase[b];
+    s_bt[b] = trim[blocks[b].j];
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = block_of_edge(s_e0, nb, e);
+    ccv[e] = ccv[e] - s_cb[b] + s_bt[b];
+  }
+}
+
 // ---- a3 auto-p: block sizes of a candidate partition without building it ---------
 // hist[i*p + j] = edges (ru, rw) with ru in V_i, rw in V_j (the nnz of block (i,j)).
 __global__ void k_part_hist(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
@@ -783,6 +834,25 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     // The batched path keeps every block's first edge in shared memory (8 B each).
     const size_t key_smem = (size_t)nb * 8;
     const bool batched = nb > 36 && key_smem <= 200 * 1024;
+    // Packed keys: cbase[b] = Σ over earlier blocks of their live column widths.
+    const uint32_t n_iso = g->n - g->n_nonisolated;   // isolated vertices: ranks [0, n_iso)
+    std::vector<uint32_t> trim(pe), cbase(nb);
+    for (uint32_t j = 0; j < pe; ++j)
+      trim[j] = plan->cuts[j] < n_iso ? std::min(plan->cuts[j + 1], n_iso) - plan->cuts[j] : 0;
+    uint64_t range = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      cbase[b] = (uint32_t)std::min<uint64_t>(range, 0xFFFFFFFFull);
+      range += plan->cuts[B.j + 1] - plan->cuts[B.j] - trim[B.j];
+    }
+    const int pbits = std::max(1, bitlen(std::max<uint64_t>(range, 1) - 1));
+    const size_t pk_smem = (size_t)nb * 16;
+    static const int packed_env = [] {   // BBTC_PACKED_TRANSPOSE = 0: never, 1: whenever it fits
+      const char* e = getenv("BBTC_PACKED_TRANSPOSE");
+      return e ? atoi(e) : -1;
+    }();
+    const bool packed = batched && range <= 0xFFFFFFFFull && pk_smem <= 48 * 1024 && packed_env != 0 &&
+                        (packed_env == 1 || (pbits + 7) / 8 < (kb + cb + 7) / 8);
     if (batched && key_smem > 48 * 1024) {
       BBTC_CUDA(cudaFuncSetAttribute(k_transpose_keys<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)key_smem));
@@ -800,6 +870,24 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
                                                  plan->ccu.p + B.e0, B.nnz, 0, bits, st);
         }, radix_kernels(B.nnz, bits));
       }
+    } else if (m && packed) {
+      DevBuf<uint32_t> keys, dcb, dtrim;
+      keys.alloc(m, ctx);
+      dcb.alloc(nb, ctx);
+      dtrim.alloc(pe, ctx);
+      BBTC_CUDA(cudaMemcpyAsync(dcb.p, cbase.data(), nb * 4, cudaMemcpyHostToDevice, st));
+      BBTC_CUDA(cudaMemcpyAsync(dtrim.p, trim.data(), pe * 4, cudaMemcpyHostToDevice, st));
+      k_transpose_keys_packed<<<grid_for(ctx, m), kThreads, pk_smem, st>>>(plan->cols.p, m, plan->d_blocks.p, nb,
+                                                                          dcb.p, dtrim.p, pe, keys.p);
+      BBTC_LAUNCHED(ctx);
+      cub_call(ctx, [&](void* t, size_t& bb) {
+        return cub::DeviceRadixSort::SortPairs(t, bb, keys.p, plan->ccv.p, plan->rows.p, plan->ccu.p, m, 0, pbits,
+                                               st);
+      }, radix_kernels(m, pbits));
+      k_unpack_cols<<<grid_for(ctx, m), kThreads, pk_smem, st>>>(plan->ccv.p, m, plan->d_blocks.p, nb, dcb.p,
+                                                                dtrim.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaStreamSynchronize(st));   // cbase / trim (host vectors) feed async copies
     } else if (m && kb + cb <= 32) {
       DevBuf<uint32_t> keys;
       keys.alloc(m, ctx);

@@ -387,3 +387,30 @@ def test_auto_p_from_budget(ctx):
     with pytest.raises(bb.BBTCError) as ei:
         bb.auto_p(ctx, g, 1000)
     assert ei.value.code == -5
+
+
+def test_packed_transpose_keys(gpu):
+    """Packed transpose keys (per-block column ranges minus the isolated prefix of each
+    part): forced on, with isolated vertices spanning several parts of user cuts."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s, d = inputs.rmat(14, 16, 6)
+    n = 1 << 16                                   # 3/4 of the ids isolated (lowest ranks)
+    og = oracle.OracleGraph(s, d, n)
+    n_iso = int((og.degrees() == 0).sum())
+    cuts_user = np.unique(np.concatenate([[0], np.linspace(0, n_iso + 2000, 9).astype(np.int64),
+                                          np.linspace(n_iso + 2000, og.n, 8).astype(np.int64), [og.n]]))
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import inputs, paper_2009_12457_b200 as bb\n"
+            "s, d = inputs.rmat(14, 16, 6); ctx = bb.Context(0); g = bb.Graph.from_edges(ctx, s, d, %d)\n"
+            "out = []\n"
+            "for p, cuts in ((16, None), (12, None), (None, %s)):\n"
+            "    plan = bb.Plan(ctx, g, p or 1, None if cuts is None else np.array(cuts, np.uint32))\n"
+            "    t, pt = plan.count(); out.append([t, pt.tolist(), plan.cuts().tolist()])\n"
+            "print(json.dumps(out))\n") % (root, n, cuts_user.tolist())
+    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1"},
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    for tot, pt, cuts in json.loads(res.stdout.strip().splitlines()[-1]):
+        otot, opt, _, _ = og.count(cuts=np.asarray(cuts, np.uint32))
+        assert tot == otot and pt == [int(x) for x in opt]
