@@ -8,4 +8,6 @@ for pk in 1 0; do
   done
 done
 done
+
+timeout 600 python scripts/stream_probe.py rmat24 2>&1 | grep "\"copy_streams\": 2" >> gpurun_out/r1z5/stream_rmat24.jsonl
 echo done

@@ -197,8 +197,9 @@ def test_device_input_streaming_and_ranks(ctx, row_major):
     # the blocks' device form); row-major blocks travel as they are
     info = plan.info()
     assert tm["h2d_bytes"] == info["stream_bytes"]
+    # (and the leading zero run of every block's row offsets is set on the device)
     if row_major:
-        assert info["stream_bytes"] == info["block_bytes"]
+        assert info["stream_bytes"] <= info["block_bytes"]
     else:
         assert info["stream_bytes"] < info["block_bytes"]
     tot3, pt3, tm3 = plan.count(timing=True)           # now resident: no copies
