@@ -321,7 +321,7 @@ struct Streamer {
   // the mapped pinned arena by the expansion kernel on the copy stream, which writes
   // the device ccv before the ready flag.
   void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst,
-            bool expand = false) {
+            bool expand = false, bool zero_runs = false) {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
@@ -337,11 +337,12 @@ struct Streamer {
       ctx->launches++;
       bytes += ((uint64_t)ncols + 1) * 4;
     }
-    // Row offsets: the block's leading run of zeros (rows before its first non-empty
-    // row — at least the isolated vertices, which hold the lowest ranks) is set on the
-    // device instead of crossing PCIe.
-    const uint64_t z = plan->rp_zero.empty() ? 0 : std::min<uint64_t>(plan->rp_zero[b], rlen);
-    if (z) BBTC_CUDA(cudaMemsetAsync(dev_rowptr + ro_dst, 0, z * 4, cs));
+    // Row offsets: with zero_runs the destination arena was zeroed before the copies
+    // (prezero_rowptr), so the block's leading run of zeros (rows before its first
+    // non-empty row — at least the isolated vertices, which hold the lowest ranks)
+    // does not cross PCIe.  (No memset here: a memset kernel on a copy stream may not
+    // find room next to the persistent count kernel that waits for this block's flag.)
+    const uint64_t z = (zero_runs && !plan->rp_zero.empty()) ? std::min<uint64_t>(plan->rp_zero[b], rlen) : 0;
     if (rlen > z)
       BBTC_CUDA(cudaMemcpyAsync(dev_rowptr + ro_dst + z, plan->h_rowptr + B.ro + z, (rlen - z) * 4,
                                 cudaMemcpyHostToDevice, cs));
@@ -362,9 +363,23 @@ struct Streamer {
     uint32_t* dev[3];
     auto arenas = plan->edge_arenas();
     for (size_t x = 0; x < arenas.size(); ++x) dev[x] = arenas[x].dev->p;
-    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro, !getenv("BBTC_NO_COLPTR"));
+    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro, !getenv("BBTC_NO_COLPTR"), zero_runs);
   }
+  bool zero_runs = false;   // the full rowptr arena was zeroed first (prezero_rowptr)
 };
+
+// Zeroes the plan's device row-offset arena on the context stream and makes the copy
+// streams wait for it, so streamed copies can skip every block's leading zero run.
+static void prezero_rowptr(bbtc_ctx* ctx, bbtc_plan* plan, Streamer* s) {
+  if (getenv("BBTC_NO_RP_ZERO")) return;
+  BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0, plan->rowptr.bytes(), ctx->stream));
+  cudaEvent_t go;
+  BBTC_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+  BBTC_CUDA(cudaEventRecord(go, ctx->stream));
+  for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, go, 0));
+  cudaEventDestroy(go);
+  s->zero_runs = true;
+}
 
 constexpr uint32_t kEpochs = 1u << 16;
 
@@ -694,6 +709,7 @@ BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (plan->resident) return;
     ensure_device_arenas(ctx, plan);
     Streamer s(ctx, plan);
+    prezero_rowptr(ctx, plan, &s);
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) s.issue(b);
     for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamSynchronize(cs));
     plan->resident = true;
@@ -928,6 +944,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       const bool greedy = !(so && std::string(so) == "exec");
       if (greedy) stream_order(ctx, plan);
       Streamer s(ctx, plan);
+      prezero_rowptr(ctx, plan, &s);   // (queued before the count kernel, so it runs first)
       s.epoch = epoch;
       for (const TaskDesc& T : greedy ? plan->s_tasks : plan->tasks) {
         s.issue(T.ij);
