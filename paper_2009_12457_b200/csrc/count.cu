@@ -206,7 +206,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
   uint32_t* tab = smem + wid * kTable;
   uint4* tab4 = reinterpret_cast<uint4*>(tab);
   uint2* pay = reinterpret_cast<uint2*>(smem + kWarps * kTable) + wid * 32;
-  uint32_t verified = 0xFFFFFFFFu;   // streaming: last task whose blocks this warp saw ready
 
   for (;;) {
     unsigned long long it = 0;
@@ -221,10 +220,8 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const TaskDesc T = tasks[lo];
-    if (ready && lo != verified) {
+    if (ready) {
       // Streaming (a6): wait until the copy engine has delivered the task's blocks.
-      // Once per task per warp: consecutive items of a task need no new acquire (the
-      // GPU-scope acquire loads are not free, and there are ~384 items per warp slot).
       if (lane == 0) {
         const uint32_t need[3] = {T.ij, T.ik, T.jk};
         for (int x = 0; x < 3; ++x) {
@@ -240,7 +237,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         }
       }
       __syncwarp();
-      verified = lo;
     }
     const BlockDesc Bij = blocks[T.ij];
     const BlockDesc BS = blocks[kCol ? T.jk : T.ik];   // block of the staged lists
