@@ -792,10 +792,11 @@ BBTC_API bbtc_status bbtc_task_ijk(uint32_t p, uint64_t idx, uint32_t* i, uint32
   });
 }
 
-// Streaming order (a6): the sparse tasks reordered so that the blocks copied first
-// unlock the most work.  Greedy: every task whose blocks are all issued goes next (in
-// execution order); otherwise the task with the most work (work items, which carry
-// equal estimated work, R8) per byte of its blocks still to copy.  The copies follow
+// Streaming order (a6): the sparse tasks reordered by when their blocks land.  Default
+// ("peel", below): the block order is built backwards so that the work left after the
+// last copies is small.  "greedy": forwards — every task whose blocks are all issued
+// goes next (in execution order); otherwise the task with the most work (work items,
+// which carry equal estimated work, R8) per byte of its blocks still to copy.  The copies follow
 // the same order, so the kernel always has unlocked work while later blocks are in
 // flight (the execution order puts the densest column of blocks last: with it the
 // kernel idles until those copies land).  O(T^2): plans with more than kGreedyMax
@@ -806,7 +807,45 @@ static void stream_order(bbtc_ctx* ctx, bbtc_plan* plan) {
   const size_t ns = plan->dense_task_lo;
   std::vector<uint32_t> ord;
   ord.reserve(ns);
-  if (ns <= kGreedyMax) {
+  static const bool peel = [] {   // default; BBTC_STREAM_ORDER=greedy selects the forward greedy order
+    const char* e = getenv("BBTC_STREAM_ORDER");
+    return !(e && std::string(e) == "greedy");
+  }();
+  if (peel && ns <= kGreedyMax) {
+    // Tail-aware: build the block order backwards.  Repeatedly take, among the blocks
+    // not yet placed, the one whose still-unplaced tasks carry the least work per byte
+    // and place it last (with those tasks): the work that can only start after the last
+    // copies land is as small as possible.  Tasks run in the order their last block lands.
+    const uint32_t nb = (uint32_t)plan->blocks.size();
+    std::vector<double> bytes(nb);
+    for (uint32_t b = 0; b < nb; ++b) bytes[b] = std::max(1.0, (double)Streamer(ctx, plan).block_bytes(b));
+    std::vector<char> gone(nb, 0), placed(ns, 0);
+    std::vector<std::vector<uint32_t>> rev_tasks;   // per peeled block, its tasks
+    for (uint32_t it = 0; it < nb; ++it) {
+      std::vector<double> w(nb, 0.0);
+      for (size_t t = 0; t < ns; ++t) {
+        if (placed[t]) continue;
+        const TaskDesc& T = plan->tasks[t];
+        const double wt = (double)(plan->item_start[t + 1] - plan->item_start[t]);
+        for (uint32_t b : {T.ij, T.ik, T.jk}) w[b] += wt;
+      }
+      int64_t best = -1;
+      for (uint32_t b = 0; b < nb; ++b)
+        if (!gone[b] && (best < 0 || w[b] / bytes[b] < w[best] / bytes[best])) best = b;
+      gone[best] = 1;
+      rev_tasks.emplace_back();
+      for (size_t t = 0; t < ns; ++t) {
+        if (placed[t]) continue;
+        const TaskDesc& T = plan->tasks[t];
+        if (T.ij == (uint32_t)best || T.ik == (uint32_t)best || T.jk == (uint32_t)best) {
+          placed[t] = 1;
+          rev_tasks.back().push_back((uint32_t)t);
+        }
+      }
+    }
+    for (size_t x = rev_tasks.size(); x-- > 0;)
+      for (uint32_t t : rev_tasks[x]) ord.push_back(t);
+  } else if (ns <= kGreedyMax) {
     const uint32_t nb = (uint32_t)plan->blocks.size();
     std::vector<double> bytes(nb);
     for (uint32_t b = 0; b < nb; ++b) bytes[b] = (double)Streamer(ctx, plan).block_bytes(b);
@@ -940,7 +979,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       ensure_device_arenas(ctx, plan);
       const uint32_t epoch = next_epoch(ctx, plan);
       copies_after_stream();
-      const char* so = getenv("BBTC_STREAM_ORDER");
+      const char* so = getenv("BBTC_STREAM_ORDER");   // exec | greedy | (default) peel
       const bool greedy = !(so && std::string(so) == "exec");
       if (greedy) stream_order(ctx, plan);
       Streamer s(ctx, plan);
