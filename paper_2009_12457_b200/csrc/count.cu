@@ -532,7 +532,8 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
       case 32: acc = dense_edges<32>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
       case 64: acc = dense_edges<64>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
       case 128: acc = dense_edges<128>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      default: acc = dense_edges<256>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 256: acc = dense_edges<256>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      default: acc = dense_edges<512>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
     }
     const uint32_t s = __reduce_add_sync(kFull, acc);
     if (lane == 0 && s) {

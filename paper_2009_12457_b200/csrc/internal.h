@@ -99,9 +99,9 @@ struct bbtc_ctx {
   size_t cache_limit = 0;
 };
 constexpr int kCursorSlots = 1024;
-constexpr uint32_t kDenseMinS = 8;     // bit-row strides (words): powers of two in [8, 256]
-constexpr uint32_t kDenseMaxS = 256;
-constexpr uint32_t kDenseBitsDefault = 2048;
+constexpr uint32_t kDenseMinS = 8;     // bit-row strides (words): powers of two in [8, 512]
+constexpr uint32_t kDenseMaxS = 512;
+constexpr uint32_t kDenseBitsDefault = 8192;
 constexpr uint32_t kAutoPMax = 256;
 constexpr uint32_t kBitmapMaxWords = 1024;   // = the count kernel's per-warp table (kTable)   // largest p the automatic choice tries
 

@@ -40,7 +40,7 @@ for p in ps:
         c.record(stream)
         tot = int(counts[-1].item())
         if it == 0:
-            info = plan.info()
+            info = plan.info()   # (dense_bytes is set once the bit rows exist: after the count)
         else:
             res.append((a.elapsed_time(b), b.elapsed_time(c)))
         plan.close()
@@ -51,4 +51,5 @@ for p in ps:
                       "step_ms": prep + cnt, "edges_per_s": info["m"] / ((prep + cnt) / 1e3),
                       "b_alg_GBps": info["b_alg"] / cnt / 1e6, "visits": info["visits"], "lambda": info["lambda"],
                       "dmax_blk": info["dmax_blk"], "block_bytes": info["block_bytes"],
-                      "sum_a": info["sum_a"], "sum_b": info["sum_b"]}), flush=True)
+                      "sum_a": info["sum_a"], "sum_b": info["sum_b"], "dense_tasks": info["dense_tasks"],
+                      "dense_bytes": info["dense_bytes"]}), flush=True)
