@@ -309,62 +309,62 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         if (L == 32 && __all_sync(kFull, valid && key == k0)) {
           if constexpr (kRunPipe && (!kBm || BBTC_RUN_PIPE_BM)) {
-          // Two-stage pipeline over the run's batches: while batch t is probed, the row
-          // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
-          // ids of batch t+2 are in flight.  Only in the hash-only variant: measured
-          // friendster -2%, while the bitmap variant (tighter on registers) lost 1.6% on
-          // rmat24 (profiles/r01c/ab_run_pipe.jsonl).
-          auto edge = [&](uint64_t e, uint32_t& pid2) {
-            const bool ok = e < e_end && (kCol ? it_v[e] : it_u[e]) == k0;
-            pid2 = ok ? (kCol ? it_u[e] : it_v[e]) : 0u;
-            return ok;
-          };
-          uint64_t e2 = base + L + lane;
-          uint32_t p_cur, p_nxt;
-          bool ok_cur = edge(e2, p_cur);
-          bool ok_nxt = edge(e2 + 32, p_nxt);
-          uint32_t b2 = 0, bl2 = 0;
-          if (ok_cur && alen > 0) {
-            b2 = rpP[p_cur];
-            bl2 = rpP[p_cur + 1] - b2;
-          }
-          for (;;) {
-            const int L2 = __popc(__ballot_sync(kFull, ok_cur));   // the run's edges: a lane prefix
-            if (L2 == 0) break;
-            uint32_t bn = 0, bln = 0, p_nn = 0;
-            bool ok_nn = false;
-            if (L2 == 32) {
-              if (ok_nxt && alen > 0) {
-                bn = rpP[p_nxt];
-                bln = rpP[p_nxt + 1];
-              }
-              ok_nn = edge(e2 + 64, p_nn);
-            }
-            hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
-            L += L2;
-            if (L2 < 32) break;
-            e2 += 32;
-            ok_cur = ok_nxt;
-            b2 = bn;
-            bl2 = bln - bn;
-            ok_nxt = ok_nn;
-            p_nxt = p_nn;
-          }
-          } else {
-          for (;;) {
-            const uint64_t e2 = base + L + lane;
-            const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
-            const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
-            if (L2 == 0) break;
+            // Two-stage pipeline over the run's batches: while batch t is probed, the row
+            // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
+            // ids of batch t+2 are in flight.  Only in the hash-only variant: measured
+            // friendster -2%, while the bitmap variant (tighter on registers) lost 1.6% on
+            // rmat24 (profiles/r01c/ab_run_pipe.jsonl).
+            auto edge = [&](uint64_t e, uint32_t& pid2) {
+              const bool ok = e < e_end && (kCol ? it_v[e] : it_u[e]) == k0;
+              pid2 = ok ? (kCol ? it_u[e] : it_v[e]) : 0u;
+              return ok;
+            };
+            uint64_t e2 = base + L + lane;
+            uint32_t p_cur, p_nxt;
+            bool ok_cur = edge(e2, p_cur);
+            bool ok_nxt = edge(e2 + 32, p_nxt);
             uint32_t b2 = 0, bl2 = 0;
-            if (ok && alen > 0) {
-              const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
-              b2 = rpP[p2];
-              bl2 = rpP[p2 + 1] - b2;
+            if (ok_cur && alen > 0) {
+              b2 = rpP[p_cur];
+              bl2 = rpP[p_cur + 1] - b2;
             }
-            hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
-            L += L2;
-            if (L2 < 32) break;
+            for (;;) {
+              const int L2 = __popc(__ballot_sync(kFull, ok_cur));   // the run's edges: a lane prefix
+              if (L2 == 0) break;
+              uint32_t bn = 0, bln = 0, p_nn = 0;
+              bool ok_nn = false;
+              if (L2 == 32) {
+                if (ok_nxt && alen > 0) {
+                  bn = rpP[p_nxt];
+                  bln = rpP[p_nxt + 1];
+                }
+                ok_nn = edge(e2 + 64, p_nn);
+              }
+              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
+              L += L2;
+              if (L2 < 32) break;
+              e2 += 32;
+              ok_cur = ok_nxt;
+              b2 = bn;
+              bl2 = bln - bn;
+              ok_nxt = ok_nn;
+              p_nxt = p_nn;
+            }
+          } else {
+            for (;;) {
+              const uint64_t e2 = base + L + lane;
+              const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
+              const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
+              if (L2 == 0) break;
+              uint32_t b2 = 0, bl2 = 0;
+              if (ok && alen > 0) {
+                const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
+                b2 = rpP[p2];
+                bl2 = rpP[p2 + 1] - b2;
+              }
+              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
+              L += L2;
+              if (L2 < 32) break;
           }
           }
         }
