@@ -500,7 +500,10 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
 }
 
 // One warp per work item of a dense task (TaskDesc.pad = the bit-row stride of V_k).
-__global__ void __launch_bounds__(kWarps * 32, 4)
+#ifndef BBTC_DENSE_MIN_CTAS
+#define BBTC_DENSE_MIN_CTAS 4
+#endif
+__global__ void __launch_bounds__(kWarps * 32, BBTC_DENSE_MIN_CTAS)
 k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
               const uint32_t* __restrict__ dense, const uint64_t* __restrict__ off,
               const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
