@@ -256,7 +256,14 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
 /* a6-a8, synchronous.  Like bbtc_count_async but returns results in HOST
  * memory: *total and (if per_task != NULL) per_task[n_tasks].  Blocks that are
  * in pinned host memory and not resident are streamed host->device on the copy
- * streams, overlapped with the kernels of earlier tasks.  t may be NULL. */
+ * streams, overlapped with ONE count kernel whose warps wait on per-block ready
+ * flags (Alg. 7's asyncCopy/isCopied).  Tasks and copies follow a
+ * tail-aware order (blocks placed last-first by least remaining work per byte), so a
+ * rank's share of work items differs from the resident mode's (sums over ranks do
+ * not).  Column-major blocks cross PCIe with per-block column offsets instead of
+ * per-edge column ids, and without the leading zero run of their row offsets
+ * (bbtc_plan_info.stream_bytes).  Afterwards the blocks are resident.  t may be NULL;
+ * t->t_h2d_ms is the time until the last copy landed. */
 BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
                                 uint32_t flags, uint64_t* total, uint64_t* per_task, bbtc_timing* t);
 
