@@ -22,7 +22,11 @@ namespace {
 
 constexpr int kWarps = 8;            // warps per CTA
 constexpr int kTable = 1024;         // per-warp shared words: one hash table of 4-word buckets (4 KiB)
-constexpr int kHashCap = kTable / 4; // staged words of a shared (multi-list) table (load <= 1/4)
+#ifndef BBTC_HASH_LOAD_HALF
+#define BBTC_HASH_LOAD_HALF 0
+#endif
+constexpr bool kLoadHalf = BBTC_HASH_LOAD_HALF;   // shared multi-list tables at load <= 1/2 (else 1/4)
+constexpr int kHashCap = kLoadHalf ? kTable / 2 : kTable / 4;   // staged words of a shared (multi-list) table
 constexpr int kChunk = kTable / 2;   // staged words of a single-list table fill (load <= 1/2)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
@@ -398,7 +402,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           // ---- stage the distinct lists S of lanes [0,L) into one table
           const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
           uint32_t nb = 16;
-          while ((dense ? 2 * nb : nb) < total_a) nb <<= 1;
+          while ((dense || kLoadHalf ? 2 * nb : nb) < total_a) nb <<= 1;
           const uint32_t bmask = nb - 1;
           const int shift = 32 - (__ffs(nb) - 1);
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
