@@ -148,3 +148,25 @@ def test_graph_load_counts_karate(tmp_path, fmt):
     assert g.n == 34 and g.m == 78
     total, per_task = bb.Plan(ctx, g, 2).count()
     assert total == 45 and per_task.tolist() == [1, 11, 28, 5]
+
+
+def test_text_and_mm_roundtrip_random(tmp_path):
+    """A seeded 200 K-pair list written by numpy as TSV and as MatrixMarket reads back
+    exactly (ids up to 2^32 - 2, the largest the ABI accepts)."""
+    bb = _bb()
+    rng = np.random.default_rng(11)
+    s = rng.integers(0, 1 << 20, size=200_000, dtype=np.uint64).astype(np.uint32)
+    d = rng.integers(0, 1 << 20, size=200_000, dtype=np.uint64).astype(np.uint32)
+    s[:3] = [0xFFFFFFFE, 0, 7]
+    d[:3] = [1, 0xFFFFFFFE, 7]
+    p = tmp_path / "r.tsv"
+    np.savetxt(p, np.stack([s, d], 1), fmt="%d", delimiter="\t", header="random", comments="# ")
+    rs, rd, _ = bb.read_edges(p, "text")
+    assert np.array_equal(rs, s) and np.array_equal(rd, d)
+    n = int(max(s.max(), d.max())) + 1
+    m = tmp_path / "r.mtx"
+    with open(m, "w") as f:
+        f.write(f"%%MatrixMarket matrix coordinate integer general\n{n} {n} {len(s)}\n")
+        np.savetxt(f, np.stack([s.astype(np.uint64) + 1, d.astype(np.uint64) + 1, np.ones_like(s)], 1), fmt="%d")
+    ms, md, nh = bb.read_edges(m, "mm")
+    assert nh == n and np.array_equal(ms, s) and np.array_equal(md, d)
