@@ -46,6 +46,39 @@ def test_karate_golden():
         assert tot == 45
 
 
+def test_karate_prefix_golden_consistent():
+    """The golden prefix sums are the App. A degrees in App. A rank order (guards the fixture)."""
+    G = load("karate.json")
+    w = [G["degrees_by_id"][o] for o in G["order_new_to_old"]]
+    assert G["prefix_degrees_by_rank"] == [sum(w[:r]) for r in range(35)]
+
+
+# ---- default cut rule: closed form on regular graphs --------------------------------
+def _regular(kind, n):
+    if kind == "cycle":
+        return cycle(n)
+    if kind == "complete":
+        return [(a, b) for a in range(n) for b in range(a + 1, n)]
+    if kind == "prism":                                          # C_{n/2} x K_2, 3-regular
+        h = n // 2
+        return cycle(h) + [(h + a, h + b) for a, b in cycle(h)] + [(a, a + h) for a in range(h)]
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind,n", [("cycle", 6), ("cycle", 12), ("cycle", 35), ("complete", 9),
+                                    ("complete", 13), ("prism", 10), ("prism", 22)])
+def test_default_cuts_regular_closed_form(kind, n):
+    """For a d-regular graph P[r] = r*d, so min{r : r*d >= ceil(i*n*d/p)} = ceil(ceil(i*n*d/p)/d)
+    = ceil(i*n/p) (nested ceilings).  Exact targets (d | i*n*d/p) pin the '>=' side of the rule,
+    ragged ones pin the ceiling (SURVEY §8(c) default cut rule)."""
+    s, d = _edges(_regular(kind, n))
+    g = oracle.OracleGraph(s, d)
+    assert g.n == n
+    for p in range(1, n + 1):
+        want = [-(-i * n // p) for i in range(p + 1)]
+        assert list(g.default_cuts(p)) == want, (kind, n, p)
+
+
 # ---- P1: brute force ------------------------------------------------------------
 @pytest.mark.parametrize("seed", range(12))
 def test_bruteforce_random(seed):
@@ -246,3 +279,18 @@ def test_rmat_shape_table3():
     assert abs(V / ref["V"] - 1) < 0.01
     assert abs(g.m / ref["E"] - 1) < 0.01
     assert abs(T / ref["T"] - 1) < 0.02
+
+
+def test_vertex_count_rule():
+    """R21: n = max(n_hint, 1 + largest raw id); ids above the hint are vertices, a
+    larger hint adds isolated vertices (lowest ranks, part 0)."""
+    s, d = _edges(wheel(9))                                           # ids 0..9, 9 triangles
+    for hint, n in ((0, 10), (3, 10), (10, 10), (25, 25)):
+        g = oracle.OracleGraph(s, d, hint)
+        assert g.n == n
+        tot, pt, _, cuts = g.count(2)
+        assert tot == 9 and cuts[-1] == n
+        assert list(g.degrees()[10:]) == [0] * (n - 10)
+        assert sorted(g.rank()[10:]) == list(range(n - 10))            # isolated: lowest ranks
+    s = np.array([7], np.uint32)                                      # a self-loop still names vertex 7
+    assert oracle.OracleGraph(s, s, 2).n == 8
