@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic capture")
     ap.add_argument("--e2e-steps", type=int, default=3)
     return ap.parse_args()
 
@@ -61,13 +62,52 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config):
-    path = os.path.join(ROOT, "profiles", f"ncu_count_{config}.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+def live_traffic(cfg, p, seed, timeout=900):
+    """DRAM bytes per launch of the two count kernels, measured in THIS run: an ncu
+    subprocess (dram__bytes_read/write.sum, gpu__time_duration.sum, L2 hit rate) over
+    scripts/profile_count.py, which builds the same plan and counts twice; the second
+    count's launches are used (the first builds the bit rows).  ncu times are
+    serialised and cold-cache: only the bytes (and L2 hit rate) are taken from it."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    with tempfile.TemporaryDirectory() as tmp:
+        log = os.path.join(tmp, "ncu.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "lts__t_sector_hit_rate.pct", "--clock-control", "none", "-k", "regex:k_count", "--csv",
+               "--log-file", log, sys.executable, os.path.join(ROOT, "scripts", "profile_count.py"), cfg.name,
+               str(p), str(seed)]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        except Exception as ex:  # noqa: BLE001
+            return None, f"ncu failed: {ex}"
+        if r.returncode != 0 or not os.path.exists(log):
+            return None, f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-300:]}"
+        rows = [ln for ln in open(log) if ln.startswith('"')]
+    launches = {}
+    for row in csv.DictReader(rows):
+        try:
+            lid = int(row["ID"])
+        except (KeyError, ValueError):
+            continue
+        d = launches.setdefault(lid, {"kernel": row.get("Kernel Name", "")})
+        v = float(str(row["Metric Value"]).replace(",", ""))
+        unit = row.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                 "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+        d[row["Metric Name"]] = v * scale
+    out = {}
+    for lid in sorted(launches):           # later launches overwrite: the second count's
+        d = launches[lid]
+        kind = "dense" if "k_count_dense" in d["kernel"] else "list"
+        out[kind] = {"dram_bytes": d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0),
+                     "dram_read_bytes": d.get("dram__bytes_read.sum", 0),
+                     "ncu_ms": d.get("gpu__time_duration.sum"), "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct"),
+                     "launch_id": lid}
+    return out, "ncu " + " ".join(cmd[1:9])
 
 
 class Clocks:
@@ -119,35 +159,33 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(cfg, s, d, threads_hint=0, target_s=8.0):
-    """The oracle as it stands, on the box's host cores, on a bounded sample:
-    full oracle preprocessing (canonicalise, rank, orient) + the node-iterator
-    count on every stride-th row, extrapolated to all rows."""
+def cpu_baseline(cfg, s, d, p):
+    """The oracle as it stands, on the box's host cores, on the WHOLE workload (not
+    extrapolated): oracle build (canonicalise, rank, orient) + its full per-task count
+    at the config's p.  edges/s = m / (build + count), like the GPU step (a1-a7)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     t0 = time.perf_counter()
-    og = oracle.OracleGraph(s, d, cfg.n_hint, threads_hint)
+    og = oracle.OracleGraph(s, d, cfg.n_hint)
     t_build = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    tot, _, _, _ = og.count(p)
+    t_count = time.perf_counter() - t1
     m = og.m
-    stride = 1024
-    t_s = 0.0
-    while True:
-        t1 = time.perf_counter()
-        og.count_rows(0, og.n, stride)
-        t_s = time.perf_counter() - t1
-        if t_s * 2 > target_s or stride == 1:
-            break
-        stride = max(1, stride // 4)
-    t_full = t_build + t_s * stride
     del og
-    return {"value": m / t_full, "unit": "edges/s", "cores": cores, "kind": "oracle",
-            "sample": f"{cfg.name}: full oracle build ({t_build:.2f} s) + node-iterator count on every "
-                      f"{stride}-th row ({t_s:.2f} s), extrapolated x{stride}",
-            "t_build_s": t_build, "t_count_sample_s": t_s, "stride": stride, "t_extrapolated_s": t_full}
+    return {"value": m / (t_build + t_count), "unit": "edges/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cfg.name}: the whole workload, not extrapolated: oracle build ({t_build:.2f} s) + full "
+                      f"per-task count at p={p} ({t_count:.2f} s) on {cores} threads",
+            "t_build_s": t_build, "t_count_s": t_count, "triangles": tot}
 
 
 def run_reference(args):
-    """--impl reference: the oracle, on rank 0 only, on this config."""
+    """--impl reference: the oracle (this tier has no reference code), rank 0 only.
+    The oracle graph is built once (timed); the K timed steps are K contiguous row
+    ranges of equal edge count — a partition of the rows, so the K steps together are
+    exactly one full node-iterator count (nothing extrapolated; strided row samples
+    were measured to inflate the time by 1.4-2x: cache locality and serial tails).
+    value = m / (build + sum of the K step times); W warm-up steps repeat pieces untimed."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -158,34 +196,33 @@ def run_reference(args):
     t0 = time.perf_counter()
     og = oracle.OracleGraph(s, d, cfg.n_hint)
     t_build = time.perf_counter() - t0
-    # stride sized so one sample step is ~2 s of CPU work
-    stride = 256
-    for _ in range(8):
+    del s, d
+    row, _ = og.csr()
+    K = max(1, args.steps)
+    cuts = np.searchsorted(row, np.linspace(0, og.m, K + 1), side="left").astype(np.int64)
+    cuts[0], cuts[-1] = 0, og.n
+    cuts = np.maximum.accumulate(cuts)
+    del row
+    for w in range(args.warmup):
+        k = w % K
+        og.count_rows(int(cuts[k]), int(cuts[k + 1]), 1)
+    times, tri = [], 0
+    for k in range(K):
         t1 = time.perf_counter()
-        og.count_rows(0, og.n, stride)
-        ts = time.perf_counter() - t1
-        if ts > 1.0 or stride == 1:
-            break
-        stride = max(1, stride // 4)
-    for _ in range(args.warmup):
-        og.count_rows(0, og.n, stride)
-    times = []
-    for k in range(args.steps):
-        t1 = time.perf_counter()
-        og.count_rows(k % stride, og.n, stride)
+        tri += og.count_rows(int(cuts[k]), int(cuts[k + 1]), 1)[0]
         times.append(time.perf_counter() - t1)
-    t_step = t_build + statistics.median(times) * stride
-    v = og.m / t_step
+    t_all = t_build + sum(times)
+    v = og.m / t_all
+    sample = (f"{cfg.name}: the whole workload as {K} contiguous row ranges of equal edge count (one full "
+              f"node-iterator count, {sum(times):.2f} s) + oracle build once ({t_build:.2f} s), {cores} threads")
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "edges/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_all / K * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": cfg.name, "desc": cfg.desc, "p": cfg.p, "seed": args.seed,
+            "config": {"workload": cfg.name, "desc": cfg.desc, "p": args.p or cfg.p, "seed": args.seed,
                        "l2": "inputs larger than L2 (CPU run)"},
             "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cores, "kind": "oracle",
-                             "sample": f"oracle build once ({t_build:.2f} s) + per step the node-iterator count "
-                                       f"on every {stride}-th row, extrapolated x{stride}"},
-            "gpu_launches": 0}
+            "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "triangles": int(tri), "step_s": times, "t_build_s": t_build, "gpu_launches": 0}
     print(json.dumps(line), flush=True)
 
 
@@ -341,10 +378,41 @@ def main():
     plan.close()
     g.close()
 
+    t_list = statistics.median(r[2]["t_kernel_ms"] - r[2]["t_dense_ms"] for r in reps_x)
+    t_dense = statistics.median(r[2]["t_dense_ms"] for r in reps_x)
+    del ds, dd
+    torch.cuda.synchronize()
+    ctx.close()
+    torch.cuda.empty_cache()
+
     peak, peak_src = load_peaks()
-    b_alg_launch = pinfo["b_alg"] / world
-    achieved = b_alg_launch / (kern / 1e3) / 1e9
-    traffic = ncu_traffic(cfg.name)
+    # Roofline of the dominant kernel (the list kernel), physical: DRAM bytes per launch
+    # measured by ncu in this run / the launch's CUDA-event time (median of the 5 counts
+    # above) / the measured HBM peak.  compulsory_* = the bytes the kernel must read at
+    # least once (the distinct blocks it reads; for the bit-row kernel the bit rows and
+    # its G_ij iteration arrays); b_alg_* = SURVEY 8(d)'s logical bytes (Alg. 5 reading
+    # both lists of every edge), which staged-list reuse and bit rows undercut.
+    traffic, traffic_src = (None, "skipped (N>1: ncu on one GPU only)")
+    if rank == 0 and world == 1 and not args.no_ncu:
+        traffic, traffic_src = live_traffic(cfg, p, args.seed)
+
+    def kern_roof(kind, t_ms, compulsory, b_alg=None):
+        tr = (traffic or {}).get(kind) if traffic else None
+        d = {"kernel_ms": t_ms, "compulsory_bytes": compulsory,
+             "compulsory_GBps": compulsory / (t_ms / 1e3) / 1e9 if t_ms > 0 else None}
+        d["compulsory_frac"] = d["compulsory_GBps"] / peak if t_ms > 0 else None
+        if tr:
+            d.update({"traffic": tr["dram_bytes"], "achieved": tr["dram_bytes"] / (t_ms / 1e3) / 1e9,
+                      "l2_hit_pct": tr["l2_hit_pct"], "ncu_ms_cold_serialised": tr["ncu_ms"],
+                      "traffic_over_compulsory": tr["dram_bytes"] / compulsory if compulsory else None})
+            d["frac"] = d["achieved"] / peak
+        if b_alg is not None:
+            d["b_alg_bytes"] = b_alg
+            d["b_alg_logical_frac"] = b_alg / (t_ms / 1e3) / 1e9 / peak if t_ms > 0 else None
+        return d
+
+    lst = kern_roof("list", t_list, dinfo["list_read_bytes"], pinfo["b_alg"] / world)
+    dns = kern_roof("dense", t_dense, dinfo["dense_bytes"] + dinfo["dense_edge_bytes"])
     line = {
         "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -355,15 +423,14 @@ def main():
         "e2e": {"value": m / (e2e / 1e3), "unit": "edges/s", "ms_per_step": e2e,
                 "h2d_bytes_per_step": 8 * E, "d2h_bytes_per_step": 8 * (nt + 1)},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_count + k_count_dense", "kernel_ms": kern,
-                     "b_alg_bytes_per_launch": b_alg_launch, "peak_source": peak_src,
-                     "note": "one count = the list kernel (k_count, sparse tasks) then the bit-row kernel "
-                             "(k_count_dense, dense tasks), timed together. achieved/frac are logical (B_alg = "
-                             "bytes Alg. 5 reads per edge, SURVEY 8(d)); staged lists reused across a run of "
-                             "edges and bit rows replacing long lists let it exceed 1. physical_frac = ncu DRAM "
-                             "bytes of both kernels per count / this time / peak.",
-                     "physical_frac": (traffic / world / (kern / 1e3) / 1e9 / peak) if traffic else None},
+        "roofline": {"bound": "hbm", "kernel": "k_count (list kernel, sparse tasks)", "unit": "GB/s", "peak": peak,
+                     "achieved": lst.get("achieved"), "frac": lst.get("frac"), "traffic": lst.get("traffic"),
+                     "compulsory_frac": lst["compulsory_frac"], "peak_source": peak_src,
+                     "traffic_source": traffic_src, "kernels": {"list": lst, "dense": dns},
+                     "note": "physical: achieved = ncu DRAM bytes (read+write) per launch, measured in this run, "
+                             "/ the launch's CUDA-event time; compulsory_frac = distinct bytes the kernel must read "
+                             "/ time / peak; b_alg_logical_frac = SURVEY 8(d) B_alg / time / peak (logical, can "
+                             "exceed 1)."},
         "clocks": clk.summary(),
         "triangles": tot,
         "paper_split": {
@@ -380,9 +447,8 @@ def main():
         "breakdown_ms": {"step": ms, "step_median": statistics.median(per_step), "step_min": min(per_step),
                          "graph_a1_a2": t_graph, "plan_a3_a5": t_plan,
                          "count_kernel": kern, "prep_and_plan": ms - kern,
-                         "count_list_kernel": tm_x["t_kernel_ms"] - tm_x["t_dense_ms"],
-                         "count_dense_kernel": tm_x["t_dense_ms"], "dense_tasks": dinfo["dense_tasks"],
-                         "dense_bit_row_bytes": dinfo["dense_bytes"],
+                         "count_list_kernel": t_list, "count_dense_kernel": t_dense,
+                         "dense_tasks": dinfo["dense_tasks"], "dense_bit_row_bytes": dinfo["dense_bytes"],
                          "count_excl_h2d": statistics.median(t_x), "count_incl_h2d": statistics.median(t_i),
                          "h2d_bytes_blocks": tm_i["h2d_bytes"],
                          "count_out_of_core_half_budget": tm_o["t_total_ms"], "h2d_bytes_out_of_core": tm_o["h2d_bytes"],
@@ -393,7 +459,7 @@ def main():
                          "(P:1182-1186); Friendster 3.133 s = 5.8e8 edges/s (P:1200-1204). Other hardware.",
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, hs.numpy().view(np.uint32), hd.numpy().view(np.uint32))
+        line["cpu_baseline"] = cpu_baseline(cfg, hs.numpy().view(np.uint32), hd.numpy().view(np.uint32), p)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

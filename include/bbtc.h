@@ -76,6 +76,11 @@ BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out);
 BBTC_API void bbtc_ctx_free(bbtc_ctx* ctx);
 /* Blocks until all work enqueued on the context has finished. */
 BBTC_API bbtc_status bbtc_ctx_sync(bbtc_ctx* ctx);
+/* *stream = the cudaStream_t every call on this context enqueues on (the caller's
+ * opts->stream, or the library-created one), so a caller can order its own work
+ * (e.g. a collective over the counters) after an asynchronous count.
+ * Errors: BBTC_EINVAL (NULL). */
+BBTC_API bbtc_status bbtc_ctx_stream(const bbtc_ctx* ctx, void** stream);
 
 /* ------------------------------------------------------------------ graph */
 #define BBTC_MEM_HOST 0
@@ -151,7 +156,7 @@ typedef struct {
   uint64_t n_blocks;        /* p(p+1)/2 upper-triangular blocks */
   uint64_t m;               /* edges (sum of block nnz) */
   uint64_t m_max;           /* largest block nnz */
-  double lambda;            /* load imbalance m_max / m_avg, m_avg = 2m/(p(p+1)) */
+  double lambda;            /* load imbalance m_max / m_avg, m_avg = 2m/(p(p+1)); 1 when m = 0 */
   uint32_t dmax_blk;        /* d'_max: largest partial degree d(G_ij,u) over all blocks */
   uint32_t host_blocks;     /* 1 if the blocks live in pinned host memory (bbtc_plan_to_host) */
   uint64_t block_bytes;     /* bytes of all blocks (row offsets + cols + row ids) */
@@ -169,6 +174,11 @@ typedef struct {
   uint64_t stream_bytes;    /* host->device bytes that bring every block to the device once
                                (bbtc_plan_to_host plans: column-major blocks cross PCIe with
                                column offsets instead of per-edge column ids); else 0 */
+  uint64_t list_read_bytes; /* compulsory reads of the list kernel: device bytes of the distinct
+                               blocks the sparse (list-kernel) tasks read */
+  uint64_t dense_edge_bytes;/* compulsory reads of the bit-row kernel besides the bit rows
+                               (dense_bytes): the per-edge iteration arrays of the distinct G_ij
+                               blocks the dense tasks walk */
 } bbtc_plan_info;
 
 #define BBTC_PLAN_STATS 1u     /* compute b_alg / visits / dmax_blk (one extra device pass) */
@@ -193,12 +203,14 @@ typedef struct {
 BBTC_API bbtc_status bbtc_plan_create(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
                                       uint32_t flags, bbtc_plan** out);
 /* a3, automatic p (p is chosen so that "three subgraphs can fit into memory
- * of the computing devices"): *p = the smallest p (1 … min(n, 256)) such that, under
+ * of the computing devices"): *p = a p in 1 … min(n, 256) such that, under
  * the default cut rule, the largest task footprint — the device bytes of the task's
  * distinct blocks (row offsets + per-edge arrays, as bbtc_plan_info.max_task_bytes
  * counts them for the given flags) — times `depth` (tasks in flight at once; 0 = 1)
- * is at most budget_bytes.  One pass over the edges per candidate p (candidates 1, 2,
- * 4, … until one fits, then the smallest fitting p below it); no blocks are built.
+ * is at most budget_bytes, searched by doubling (1, 2, 4, … until one fits) and then a
+ * linear scan of (hi/2, hi): the footprint is not monotone in p (the cuts move with
+ * p), so a smaller fitting p below hi/2 is not searched for.  One pass over the edges
+ * per candidate p; no blocks are built.
  * Use the result with bbtc_plan_create and, for a budget below the plan's bytes,
  * bbtc_plan_to_host + bbtc_plan_set_budget.
  * Errors: BBTC_EINVAL (NULL, budget 0), BBTC_ERANGE (no p <= min(n, 256) fits). */

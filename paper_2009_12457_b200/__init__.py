@@ -44,7 +44,12 @@ def _ptr(x, want_dtype):
         assert x.is_contiguous(), "tensor must be contiguous"
         assert x.dtype in (torch.int32, torch.uint32), "edge arrays must be 32-bit"
         return ctypes.c_void_p(x.data_ptr()), x.numel(), (MEM_DEVICE if x.is_cuda else MEM_HOST)
-    a = np.ascontiguousarray(x, dtype=want_dtype)
+    a = np.asarray(x)
+    if a.dtype != want_dtype:
+        # Vertex ids are u32 with 0xFFFFFFFF reserved (bbtc.h); refuse values a cast would wrap.
+        if a.size and (a.dtype.kind not in "iu" or int(a.min()) < 0 or int(a.max()) > 0xFFFFFFFE):
+            raise OverflowError("vertex ids must be integers in [0, 2^32-2]")
+    a = np.ascontiguousarray(a, dtype=want_dtype)
     return ctypes.c_void_p(a.ctypes.data), len(a), MEM_HOST, a
 
 
@@ -85,6 +90,13 @@ class Context:
 
     def sync(self):
         L.check(L.bbtc_ctx_sync(self._h))
+
+    @property
+    def stream(self) -> int:
+        """The cudaStream_t handle this context enqueues on (bbtc_ctx_stream)."""
+        s = ctypes.c_void_p()
+        L.check(L.bbtc_ctx_stream(self._h, ctypes.byref(s)))
+        return int(s.value or 0)
 
     @property
     def launches(self) -> int:

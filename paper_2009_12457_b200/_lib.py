@@ -55,7 +55,8 @@ class bbtc_plan_info(ctypes.Structure):
                 ("m_max", c_u64), ("lambda_", ctypes.c_double), ("dmax_blk", c_u32), ("host_blocks", c_u32),
                 ("block_bytes", c_u64), ("max_task_bytes", c_u64), ("b_alg", c_u64), ("visits", c_u64),
                 ("work_items", c_u64), ("sum_a", c_u64), ("sum_b", c_u64),
-                ("dense_tasks", c_u32), ("dense_bits", c_u32), ("dense_bytes", c_u64), ("stream_bytes", c_u64)]
+                ("dense_tasks", c_u32), ("dense_bits", c_u32), ("dense_bytes", c_u64), ("stream_bytes", c_u64),
+                ("list_read_bytes", c_u64), ("dense_edge_bytes", c_u64)]
 
 
 class bbtc_edge_list(ctypes.Structure):
@@ -78,6 +79,7 @@ _st = ctypes.c_int
 bbtc_ctx_create = _sig("bbtc_ctx_create", _st, ctypes.POINTER(bbtc_ctx_opts), _pp)
 bbtc_ctx_free = _sig("bbtc_ctx_free", None, _vp)
 bbtc_ctx_sync = _sig("bbtc_ctx_sync", _st, _vp)
+bbtc_ctx_stream = _sig("bbtc_ctx_stream", _st, _vp, ctypes.POINTER(_vp))
 bbtc_ctx_launches = _sig("bbtc_ctx_launches", c_u64, _vp)
 bbtc_graph_from_edges = _sig("bbtc_graph_from_edges", _st, _vp, _vp, _vp, c_u64, c_u32, ctypes.c_int, _pp)
 bbtc_graph_stats_get = _sig("bbtc_graph_stats_get", _st, _vp, ctypes.POINTER(bbtc_graph_stats))

@@ -274,6 +274,25 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     }
   }
   if (plan->dense_task_lo >= plan->tasks.size()) plan->dense_item_lo = plan->item_start.back();
+  {   // compulsory bytes of both kernels (roofline denominators)
+    std::vector<char> seen(plan->blocks.size(), 0), seen_d(plan->blocks.size(), 0);
+    uint64_t lb = 0, db = 0;
+    for (size_t t = 0; t < plan->tasks.size(); ++t) {
+      const TaskDesc& T = plan->tasks[t];
+      if (t < plan->dense_task_lo) {
+        for (uint32_t b : {T.ij, T.ik, T.jk})
+          if (!seen[b]) {
+            seen[b] = 1;
+            lb += bbytes(b);
+          }
+      } else if (!seen_d[T.ij]) {
+        seen_d[T.ij] = 1;
+        db += 8 * plan->blocks[T.ij].nnz;
+      }
+    }
+    plan->info.list_read_bytes = lb;
+    plan->info.dense_edge_bytes = db;
+  }
   plan->info.work_items = plan->item_start.back();
   plan->info.max_task_bytes = max_task_bytes;
   plan->info.dense_tasks = (uint32_t)(plan->tasks.size() - plan->dense_task_lo);
@@ -310,33 +329,37 @@ struct Streamer {
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
   }
+  // Column offsets a streamed copy of block b carries (0 unless ccv travels as colptr).
+  uint64_t clen(uint32_t b) const {
+    const BlockDesc& B = plan->blocks[b];
+    return plan->streams_colptr() && B.nnz ? (uint64_t)B.nc + 1 : 0;
+  }
+  // Device bytes of block b's streamed form (per-edge arenas + row and column offsets).
   uint64_t block_bytes(uint32_t b) const {
     const BlockDesc& B = plan->blocks[b];
-    return 4 * B.nnz * plan->edge_arenas().size() + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+    return 4 * B.nnz * plan->stream_edge_arenas() + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1) +
+           4 * clen(b);
   }
   // Copies block b from the pinned host arenas to device arenas (edge arrays at
-  // edge offset e_dst, row offsets at ro_dst), then its ready flag = epoch.
-  // expand: a column-major block's column ids cross PCIe as its column offsets
-  // (|V_j|+1 words instead of nnz: 8 instead of 12 bytes per edge), read straight from
-  // the mapped pinned arena by the expansion kernel on the copy stream, which writes
-  // the device ccv before the ready flag.
+  // edge offset e_dst, row offsets at ro_dst, column offsets at co_dst), then its
+  // ready flag = epoch.  A column-major block's column ids cross PCIe as its column
+  // offsets (|V_j|+1 words instead of nnz: 8 instead of 12 bytes per edge); the count
+  // kernel reads them directly (kCP).  Only copy-engine operations go on the copy
+  // streams: the persistent count kernel that waits for the flag never depends on a
+  // kernel it could starve of SMs.
   void copy(uint32_t b, uint32_t* const* dev_edges, uint32_t* dev_rowptr, uint64_t e_dst, uint64_t ro_dst,
-            bool expand = false, bool zero_runs = false) {
+            uint32_t* dev_colptr, uint64_t co_dst, bool zero_runs = false) {
     const BlockDesc& B = plan->blocks[b];
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
     auto arenas = plan->edge_arenas();
-    expand = expand && plan->colmajor && plan->hd_colptr;
-    const size_t direct = expand ? 2 : arenas.size();   // arena 2 (ccv) comes from the offsets
+    const size_t direct = plan->stream_edge_arenas();   // colptr form: arena 2 (ccv) stays home
     if (B.nnz)
       for (size_t x = 0; x < direct; ++x)
         BBTC_CUDA(cudaMemcpyAsync(dev_edges[x] + e_dst, *arenas[x].host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
-    if (expand && B.nnz) {
-      const uint32_t ncols = plan->cuts[B.j + 1] - plan->cuts[B.j];
-      colptr_expand(cs, plan->hd_colptr + plan->co_off[b], ncols, dev_edges[2] + e_dst);
-      ctx->launches++;
-      bytes += ((uint64_t)ncols + 1) * 4;
-    }
+    if (const uint64_t cl = clen(b))
+      BBTC_CUDA(cudaMemcpyAsync(dev_colptr + co_dst, plan->h_colptr + plan->co_off[b], cl * 4,
+                                cudaMemcpyHostToDevice, cs));
     // Row offsets: with zero_runs the destination arena was zeroed before the copies
     // (prezero_rowptr), so the block's leading run of zeros (rows before its first
     // non-empty row — at least the isolated vertices, which hold the lowest ranks)
@@ -349,7 +372,7 @@ struct Streamer {
     flag(b, cs);
     if (!ev[b]) BBTC_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
     BBTC_CUDA(cudaEventRecord(ev[b], cs));
-    bytes += block_bytes(b) - (direct < arenas.size() ? 4 * B.nnz : 0) - 4 * z;
+    bytes += block_bytes(b) - 4 * z;
   }
   // The ready flag is a 4-byte copy from a read-only pinned table (h_epochs[e] = e)
   // queued behind the block's copies: the copy engine writes it after the data.
@@ -363,7 +386,8 @@ struct Streamer {
     uint32_t* dev[3];
     auto arenas = plan->edge_arenas();
     for (size_t x = 0; x < arenas.size(); ++x) dev[x] = arenas[x].dev->p;
-    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro, !getenv("BBTC_NO_COLPTR"), zero_runs);
+    copy(b, dev, plan->rowptr.p, plan->blocks[b].e0, plan->blocks[b].ro, plan->d_colptr.p,
+         plan->co_off.empty() ? 0 : plan->co_off[b], zero_runs);
   }
   bool zero_runs = false;   // the full rowptr arena was zeroed first (prezero_rowptr)
 };
@@ -459,6 +483,15 @@ static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
   if (!plan->rowptr.p) plan->rowptr.alloc(rowptr_len(plan), ctx);
   for (auto& A : plan->edge_arenas())
     if (!A.dev->p && plan->m) A.dev->alloc(plan->m, ctx);
+  if (plan->streams_colptr() && !plan->d_colptr.p) plan->d_colptr.alloc(std::max<uint64_t>(plan->co_off.back(), 1), ctx);
+}
+
+// After streamed copies into the plan's full arenas have landed (context stream, which
+// waited for them): ccv from the column offsets, so the plan is fully resident again.
+static void finish_full_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
+  if (!plan->streams_colptr()) return;
+  colptr_expand_all(ctx, plan);
+  plan->d_colptr.reset();
 }
 
 }  // namespace bbtc
@@ -531,6 +564,13 @@ BBTC_API bbtc_status bbtc_ctx_sync(bbtc_ctx* c) {
   return guard([&] {
     if (!c) raise(BBTC_EINVAL, "ctx is NULL");
     BBTC_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+BBTC_API bbtc_status bbtc_ctx_stream(const bbtc_ctx* c, void** stream) {
+  return guard([&] {
+    if (!c || !stream) raise(BBTC_EINVAL, "ctx/stream is NULL");
+    *stream = (void*)c->stream;
   });
 }
 
@@ -670,9 +710,7 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (plan->colmajor) {   // the streamed form of ccv: per-block column offsets
       DevBuf<uint32_t> cp;
       const uint64_t len = colptr_build(ctx, plan, &cp);
-      BBTC_CUDA(cudaHostAlloc((void**)&plan->h_colptr, std::max<uint64_t>(len, 1) * 4,
-                              cudaHostAllocPortable | cudaHostAllocMapped));
-      BBTC_CUDA(cudaHostGetDevicePointer((void**)&plan->hd_colptr, plan->h_colptr, 0));
+      BBTC_CUDA(cudaHostAlloc((void**)&plan->h_colptr, std::max<uint64_t>(len, 1) * 4, cudaHostAllocPortable));
       BBTC_CUDA(cudaMemcpyAsync(plan->h_colptr, cp.p, len * 4, cudaMemcpyDeviceToHost, st));
       BBTC_CUDA(cudaStreamSynchronize(st));
     }
@@ -712,6 +750,8 @@ BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan) {
     prezero_rowptr(ctx, plan, &s);
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) s.issue(b);
     for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamSynchronize(cs));
+    finish_full_arenas(ctx, plan);
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     plan->resident = true;
   });
 }
@@ -723,6 +763,7 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
     plan->rowptr.reset();
+    plan->d_colptr.reset();
     plan->dense.reset();
     plan->dense_ready = false;
     plan->resident = false;
@@ -965,13 +1006,15 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         BBTC_CUDA(cudaEventRecord(c_end.back(), cs));
       }
     };
-    uint64_t all_bytes = 0;
+    uint64_t all_bytes = 0;   // streamed form of every block
     for (uint32_t b = 0; b < plan->blocks.size(); ++b) all_bytes += Streamer(ctx, plan).block_bytes(b);
+    // the full arenas also hold ccv (expanded once the copies have landed)
+    const uint64_t full_bytes = all_bytes + (plan->streams_colptr() ? 4 * plan->m : 0);
     cudaEvent_t kmid = nullptr;
     if (plan->resident) {
       BBTC_CUDA(cudaEventCreate(&kmid));
       count_resident(ctx, plan, rank, world, d_counts.p, kmid);
-    } else if (plan->budget == 0 || plan->budget >= all_bytes) {
+    } else if (plan->budget == 0 || plan->budget >= full_bytes) {
       // a6: every block is copied on the copy streams in first-use order and then
       // flagged ready (epoch) on the device; ONE persistent count kernel runs
       // concurrently and each warp waits on the flags of its item's three blocks,
@@ -993,13 +1036,21 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       // Sparse tasks first (they come first in execution order, so their blocks are
       // issued first); the dense tasks' bit rows are built once every copy has landed
       // and the bit-row kernel runs after the list kernel, as in the resident case.
-      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch, nullptr,
+      DevArenas full;
+      full.cols = plan->cols.p;
+      full.it_u = plan->colmajor ? plan->ccu.p : plan->rows.p;
+      full.it_v = plan->colmajor ? (plan->streams_colptr() ? nullptr : plan->ccv.p) : plan->cols.p;
+      full.rowptr = plan->rowptr.p;
+      full.blocks = plan->d_blocks.p;
+      full.colptr = plan->streams_colptr() ? plan->d_colptr.p : nullptr;
+      count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch, &full,
                    greedy ? plan->d_s_tasks.p : nullptr, greedy ? plan->d_s_item_start.p : nullptr);
       // the count stream must not run past copies it did not wait for
       for (auto& e : s.ev)
         if (e) BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
       h2d = s.bytes;
       copies_done();
+      finish_full_arenas(ctx, plan);
       plan->resident = true;
       if (plan->dense_item_lo < plan->item_start.back()) {
         BBTC_CUDA(cudaEventCreate(&kmid));
@@ -1014,9 +1065,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       // ones are copied into free cache space (first fit), every block of the window
       // is flagged with the window's epoch, and the count kernel runs over the
       // window's work items, its warps waiting on the flags as in the streamed mode.
-      auto arenas = plan->edge_arenas();
-      const uint64_t A = arenas.size();
-      const uint64_t ro_all = rowptr_len(plan);
+      const uint64_t A = plan->stream_edge_arenas();
+      const bool cpf = plan->streams_colptr();
+      Streamer sz(ctx, plan);
+      uint64_t ro_all = 0;   // row offsets + (colptr form) column offsets of every block
+      for (uint32_t b = 0; b < plan->blocks.size(); ++b)
+        ro_all += (uint64_t)(plan->cuts[plan->blocks[b].i + 1] - plan->cuts[plan->blocks[b].i]) + 1 + sz.clen(b);
       const double frac_e = (double)(4 * A * plan->m) / (double)std::max<uint64_t>(all_bytes, 1);
       const uint64_t cap_e = (uint64_t)((double)plan->budget * frac_e) / (4 * A);
       const uint64_t cap_r = (plan->budget - cap_e * 4 * A) / 4;
@@ -1028,10 +1082,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       RangeAlloc ea(cap_e), ra(cap_r);
       const uint32_t nb = (uint32_t)plan->blocks.size();
       std::vector<int64_t> at_e(nb, -1), at_r(nb, -1);   // cache placement of resident blocks
-      auto rlen = [&](uint32_t b) {
+      auto rowlen = [&](uint32_t b) {
         const BlockDesc& B = plan->blocks[b];
         return (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
       };
+      // a block's offset region in the cache: row offsets, then its column offsets
+      auto rlen = [&](uint32_t b) { return rowlen(b) + sz.clen(b); };
       std::vector<DevBuf<BlockDesc>> tables;   // per-window block tables, alive until the end
       std::vector<std::vector<uint32_t>> uses(nb);   // execution-order task indices using each block
       for (uint32_t t = 0; t < plan->tasks.size(); ++t)
@@ -1146,6 +1202,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         for (uint32_t b : wblocks) {
           tab[b].e0 = (uint64_t)at_e[b];
           tab[b].ro = (uint64_t)at_r[b];
+          tab[b].co = (uint64_t)at_r[b] + rowlen(b);
         }
         tables.emplace_back();
         tables.back().alloc(nb, ctx);
@@ -1155,16 +1212,17 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         s.epoch = epoch;
         if (wait_for >= 0)
           for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamWaitEvent(cs, ev_done[wait_for], 0));
-        for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b], !getenv("BBTC_NO_COLPTR"));
+        for (uint32_t b : load) s.copy(b, dev_edges, cache_rp.p, at_e[b], at_r[b], cache_rp.p, at_r[b] + rowlen(b));
         for (uint32_t b : wblocks)
           if (std::find(load.begin(), load.end(), b) == load.end())
             s.flag(b, ctx->copy_streams[s.rr++ % ctx->copy_streams.size()]);
         DevArenas ar;
         ar.cols = dev_edges[0];
-        ar.it_u = plan->colmajor ? dev_edges[1] : dev_edges[1];
-        ar.it_v = plan->colmajor ? dev_edges[2] : dev_edges[0];
+        ar.it_u = dev_edges[1];
+        ar.it_v = plan->colmajor ? (cpf ? nullptr : dev_edges[2]) : dev_edges[0];
         ar.rowptr = cache_rp.p;
         ar.blocks = tables.back().p;
+        ar.colptr = cpf ? cache_rp.p : nullptr;
         count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[t0w], plan->item_start[t1w],
                      plan->d_ready.p, epoch, &ar);
         ev_done.emplace_back();

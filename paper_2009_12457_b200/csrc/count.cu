@@ -193,17 +193,69 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
   return hits;
 }
 
+// Streamed column-major blocks carry column offsets cp[0..nc] (block-local edge
+// offsets, cp[nc] = nnz) instead of a column id per edge.  col_search: the largest
+// c in [lo, hi) with cp[c] <= x, i.e. the column of edge x (empty columns share the
+// offset of the next one and are skipped), given cp[lo] <= x.  32-ary warp search:
+// one coalesced probe of 32 offsets per step.
+__device__ __forceinline__ uint32_t col_search(const uint32_t* __restrict__ cp, uint32_t lo, uint32_t hi, uint32_t x,
+                                               int lane) {
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) >> 5;
+    const uint32_t idx = lo + lane * step;
+    const uint32_t m = __ballot_sync(kFull, idx < hi && cp[idx] <= x);
+    lo += (31 - __clz(m)) * step;
+    hi = min(lo + step, hi);
+  }
+  const uint32_t idx = lo + lane;
+  const uint32_t m = __ballot_sync(kFull, idx < hi && cp[idx] <= x);
+  return lo + 31 - __clz(m);
+}
+
+// Column of every lane's edge (local offset x, `valid` lanes) from column offsets,
+// given a column c with cp[c] <= every lane's x: one coalesced window of the next 32
+// column ends per round, a 5-step shuffle search per lane; lanes past the window
+// restart from the column of the first of them (col_search).  Returns the column
+// (0xFFFFFFFF for invalid lanes).
+__device__ __forceinline__ uint32_t col_of(const uint32_t* __restrict__ cp, uint32_t nc, uint32_t c, uint32_t x,
+                                           bool valid, int lane) {
+  uint32_t v = 0xFFFFFFFFu;
+  bool need = valid;
+  for (;;) {
+    const uint32_t w = cp[min(c + 1 + lane, nc)];   // end of column c + lane
+    uint32_t pos = 0;
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1) {
+      const uint32_t t = __shfl_sync(kFull, w, pos + st - 1);
+      if (t <= x) pos += st;
+    }
+    if (pos == 31 && __shfl_sync(kFull, w, 31) <= x) pos = 32;
+    if (need && pos < 32) {
+      v = c + pos;
+      need = false;
+    }
+    const uint32_t un = __ballot_sync(kFull, need);
+    if (!un) break;
+    c = col_search(cp, c + 32, nc, __shfl_sync(kFull, x, __ffs(un) - 1), lane);
+  }
+  return v;
+}
+
 // Alg. 5 over work items.  kSlots: batches of several staged lists share one table
 // with slot-tagged keys (w << 5 | slot), which needs |V_k| < 2^27; otherwise every
 // batch takes one staged list at a time (long_list).  kCol: walk G_ij by column
-// (ccu/ccv arrays, stage N(G_jk,v)) or by row (rows/cols, stage N(G_ik,u)).
-template <bool kSlots, bool kCol, bool kBm>
+// (ccu/ccv arrays, stage N(G_jk,v)) or by row (rows/cols, stage N(G_ik,u)).  kCP
+// (streamed column-major blocks): the column of an edge comes from the block's column
+// offsets (colptr + BlockDesc.co) instead of a ccv array.
+template <bool kSlots, bool kCol, bool kBm, bool kCP>
 __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
         const uint32_t* __restrict__ rowptr, const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
-        unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch) {
+        unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch,
+        const uint32_t* __restrict__ colptr) {
+  static_assert(!kCP || kCol, "column offsets replace the column ids of a column-major walk");
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -250,6 +302,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     const uint32_t* rpS = rowptr + BS.ro;
     const uint32_t* cS = cols + BS.e0;
     const uint32_t* rpP = rowptr + BP.ro;
+    const uint32_t* cpb = kCP ? colptr + Bij.co : nullptr;   // G_ij's column offsets (kCP)
+    uint32_t ccol = 0;                                        // a column with cpb[ccol] <= next edge
+    if constexpr (kCP) ccol = col_search(cpb, 0, Bij.nc, (uint32_t)(e_begin - Bij.e0), lane);
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
@@ -258,7 +313,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const uint64_t e = base + lane;
       const bool valid = e < e_end;
       const uint32_t u = valid ? it_u[e] : 0xFFFFFFFFu;
-      const uint32_t v = valid ? it_v[e] : 0xFFFFFFFFu;
+      uint32_t v;
+      if constexpr (kCP) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
+      else v = valid ? it_v[e] : 0xFFFFFFFFu;
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
       uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;   // a: staged list, b: probe list
@@ -312,6 +369,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       auto continue_run = [&](auto test) {
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         if (L == 32 && __all_sync(kFull, valid && key == k0)) {
+          // kCP: the run's edges end where column k0 ends
+          const uint64_t run_end = kCP ? Bij.e0 + cpb[k0 + 1] : 0;
+          auto same = [&](uint64_t e) { return kCP ? e < run_end : (kCol ? it_v[e] : it_u[e]) == k0; };
           if constexpr (kRunPipe && (!kBm || BBTC_RUN_PIPE_BM)) {
             // Two-stage pipeline over the run's batches: while batch t is probed, the row
             // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
@@ -319,7 +379,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
             // friendster -2%, while the bitmap variant (tighter on registers) lost 1.6% on
             // rmat24 (profiles/r01c/ab_run_pipe.jsonl).
             auto edge = [&](uint64_t e, uint32_t& pid2) {
-              const bool ok = e < e_end && (kCol ? it_v[e] : it_u[e]) == k0;
+              const bool ok = e < e_end && same(e);
               pid2 = ok ? (kCol ? it_u[e] : it_v[e]) : 0u;
               return ok;
             };
@@ -357,7 +417,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           } else {
             for (;;) {
               const uint64_t e2 = base + L + lane;
-              const bool ok = e2 < e_end && (kCol ? it_v[e2] : it_u[e2]) == k0;
+              const bool ok = e2 < e_end && same(e2);
               const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
               if (L2 == 0) break;
               uint32_t b2 = 0, bl2 = 0;
@@ -416,6 +476,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           continue_run(test);
         }
       }
+      // kCP: the next batch starts after the last consumed edge, in its column or later
+      // (a continued run consumed only edges of column k0 = lane 31's column)
+      if constexpr (kCP) ccol = __shfl_sync(kFull, v, min(L, 32) - 1);
       base += L;
     }
     // one atomic pair per warp-item
@@ -625,18 +688,25 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   const bool hash = max_part < (1u << 27);
   using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
                          const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
-                         unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t);
+                         unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t,
+                         const uint32_t*);
   // The bitmap variant only where some task's V_k is small enough (it costs the main
   // loop a few registers: friendster, whose parts are all large, measured 0.7% slower).
   bool bm = false;
   for (const TaskDesc& T : plan->tasks) bm = bm || T.bmw != 0;
-  const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0) | (kBitmap && bm ? 4 : 0);
-  static const KernT kerns[8] = {k_count<false, false, false>, k_count<true, false, false>,
-                                 k_count<false, true, false>,  k_count<true, true, false>,
-                                 k_count<false, false, true>,  k_count<true, false, true>,
-                                 k_count<false, true, true>,   k_count<true, true, true>};
+  const bool cp = ar && ar->colptr && plan->colmajor;
+  const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0) | (kBitmap && bm ? 4 : 0) | (cp ? 8 : 0);
+  static const KernT kerns[16] = {
+      k_count<false, false, false, false>, k_count<true, false, false, false>,
+      k_count<false, true, false, false>,  k_count<true, true, false, false>,
+      k_count<false, false, true, false>,  k_count<true, false, true, false>,
+      k_count<false, true, true, false>,   k_count<true, true, true, false>,
+      nullptr,                             nullptr,
+      k_count<false, true, false, true>,   k_count<true, true, false, true>,
+      nullptr,                             nullptr,
+      k_count<false, true, true, true>,    k_count<true, true, true, true>};
   KernT kern = kerns[variant];
-  static int per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  static int per_sm[16] = {};
   if (!per_sm[variant]) {
     BBTC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
     // Shared-memory carveout: what the resident CTAs need, the rest stays L1 for the
@@ -667,7 +737,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
-      (uint32_t)nt, ready, epoch);
+      (uint32_t)nt, ready, epoch, ar->colptr);
   BBTC_LAUNCHED(ctx);
 }
 

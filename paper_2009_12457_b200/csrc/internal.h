@@ -124,6 +124,9 @@ struct BlockDesc {
   uint64_t nnz;     // edges
   uint64_t ro;      // first row offset (index into rowptr arena); |V_i|+1 entries
   uint32_t i, j;
+  uint64_t co;      // streamed column-major blocks: first of its |V_j|+1 column offsets (colptr arena)
+  uint32_t nc;      // columns |V_j|
+  uint32_t pad_;
 };
 
 // Task (i,j,k) as the count kernel sees it.
@@ -151,6 +154,7 @@ struct bbtc_plan {
   bbtc::DevBuf<uint32_t> rows;        // m: local row id u - cuts[i]
   bbtc::DevBuf<uint32_t> rowptr;      // sum over blocks of |V_i|+1
   bbtc::DevBuf<uint32_t> ccu, ccv;    // m: column-major iteration order (u, v) of each block
+  bbtc::DevBuf<uint32_t> d_colptr;    // streamed column-major plans: per block at co, |V_j|+1 local column offsets
   bool colmajor = true;               // kernel walks G_ij by column (ccu/ccv) vs by row (rows/cols)
   bbtc::DevBuf<BlockDesc> d_blocks;
   bbtc::DevBuf<TaskDesc> d_tasks;
@@ -168,10 +172,10 @@ struct bbtc_plan {
   uint32_t* h_ccu = nullptr;
   uint32_t* h_ccv = nullptr;
   // Streamed counts ship each column-major block's column ids as column offsets
-  // (|V_j|+1 words per block instead of nnz), read by the device from this mapped
-  // pinned arena and expanded into ccv.
+  // (|V_j|+1 words per block instead of nnz), copied by the copy engine; the count
+  // kernel finds every edge's column in them (no expansion kernel on the copy streams,
+  // so nothing the persistent count kernel waits for needs an SM).
   uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
-  uint32_t* hd_colptr = nullptr;      // the same arena's device (mapped) address
   std::vector<uint64_t> rp_zero;      // per block: leading zero entries of its row offsets
   std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
   bool resident = true;               // device arenas hold every block
@@ -207,6 +211,10 @@ struct bbtc_plan {
     if (colmajor) return {{&cols, &h_cols}, {&ccu, &h_ccu}, {&ccv, &h_ccv}};
     return {{&cols, &h_cols}, {&rows, &h_rows}};
   }
+  // The per-edge arenas a streamed copy moves: a column-major block's ccv travels as
+  // column offsets (colptr), so only cols + ccu cross per edge.
+  bool streams_colptr() const { return colmajor && h_colptr != nullptr; }
+  size_t stream_edge_arenas() const { return colmajor ? (h_colptr ? 2 : 3) : 2; }
 };
 
 namespace bbtc {
@@ -222,9 +230,10 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
 struct DevArenas {
   const uint32_t* cols = nullptr;
   const uint32_t* it_u = nullptr;
-  const uint32_t* it_v = nullptr;
+  const uint32_t* it_v = nullptr;     // per-edge column ids, or NULL with colptr
   const uint32_t* rowptr = nullptr;
   const BlockDesc* blocks = nullptr;
+  const uint32_t* colptr = nullptr;   // column offsets (BlockDesc.co / nc) instead of it_v
 };
 void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
@@ -239,7 +248,8 @@ void dense_build(bbtc_ctx* ctx, bbtc_plan* plan);
 // Column offsets of every column-major block (host plan preparation) and their
 // expansion back to per-edge column ids after a streamed copy (copy stream).
 uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, bbtc::DevBuf<uint32_t>* out);
-void colptr_expand(cudaStream_t st, const uint32_t* colptr, uint32_t ncols, uint32_t* ccv);
+// ccv of every block from the device colptr arena (context stream, after the copies).
+void colptr_expand_all(bbtc_ctx* ctx, bbtc_plan* plan);
 void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                         uint64_t item_lo, uint64_t item_hi);
 // capi.cpp (host)

@@ -382,15 +382,25 @@ __global__ void k_col_local(const BlockDesc* __restrict__ blocks, const uint64_t
       colptr[co[b] + c] -= (uint32_t)B.e0;
   }
 }
-// Expansion after a streamed copy: ccv[x] = c for every edge x of column c.  One-warp
-// CTAs with few registers, so they find room next to the persistent count kernel
-// (5 CTAs of 256 threads x <= 48 registers leave 4096 registers per SM) that waits
-// for the ready flag queued behind this kernel.
-__global__ void __launch_bounds__(32) k_col_expand(const uint32_t* __restrict__ colptr, uint32_t ncols,
-                                                   uint32_t* __restrict__ ccv) {
-  for (uint32_t c = blockIdx.x * 32 + threadIdx.x; c < ncols; c += gridDim.x * 32) {
-    const uint32_t x1 = colptr[c + 1];
-    for (uint32_t x = colptr[c]; x < x1; ++x) ccv[x] = c;
+// ccv from the column offsets once a streamed count's copies have landed (context
+// stream, ordered after the count kernel): ccv[e0 + x] = c for every edge x of column
+// c of every block.  A warp per 32 columns, lanes over a column's edges.
+__global__ void k_col_expand_all(const uint32_t* __restrict__ colptr, const BlockDesc* __restrict__ blocks,
+                                 uint32_t nb, uint32_t* __restrict__ ccv) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const BlockDesc B = blocks[b];
+    if (!B.nnz) continue;
+    const uint32_t* C = colptr + B.co;
+    uint32_t* V = ccv + B.e0;
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t c0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; c0 < B.nc; c0 += nwarps * 32) {
+      const uint32_t cn = min(32u, B.nc - c0);
+      for (uint32_t x = 0; x < cn; ++x) {
+        const uint32_t a = C[c0 + x], z = C[c0 + x + 1];
+        for (uint32_t y = a + lane; y < z; y += 32) V[y] = c0 + x;
+      }
+    }
   }
 }
 
@@ -461,7 +471,8 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   // sorted pieces are merged; the full sort no longer waits for the whole transfer.
   // At most ~8 pieces (3 merge rounds), each a whole number of 32 Mi-pair copy chunks.
   const uint64_t piece = std::max<uint64_t>(1ull << 26, ((E / 8 + (1ull << 25) - 1) >> 25) << 25);
-  bool stream_sort = !use_hash && mem == BBTC_MEM_HOST && E > piece && E < (1ull << 32) &&
+  // cub::DeviceMerge takes int lengths: every merged run (up to E keys) must stay below 2^31.
+  bool stream_sort = !use_hash && mem == BBTC_MEM_HOST && E > piece && E < (1ull << 31) &&
                      !getenv("BBTC_NO_STREAM_SORT");
   DevBuf<uint64_t> alt;
   DevBuf<uint8_t> sort_tmp;
@@ -786,6 +797,9 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       B.e0 = starts[b];
       B.nnz = starts[b + 1] - starts[b];
       B.ro = ro;
+      B.co = 0;
+      B.nc = plan->cuts[j + 1] - plan->cuts[j];
+      B.pad_ = 0;
       ro += (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
       m_max = std::max(m_max, B.nnz);
       bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1);
@@ -924,7 +938,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   plan->info.n_blocks = nb;
   plan->info.m = m;
   plan->info.m_max = m_max;
-  plan->info.lambda = m ? (double)m_max / (2.0 * (double)m / ((double)pe * (pe + 1))) : 0.0;
+  plan->info.lambda = m ? (double)m_max / (2.0 * (double)m / ((double)pe * (pe + 1))) : 1.0;   // S: lambda >= 1, = 1 when empty
   plan->info.block_bytes = bytes;
   {
     const char* e = getenv("BBTC_DENSE_BITS");
@@ -970,15 +984,21 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
     k_col_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dco.p, nb, dcuts.p, out->p);
     BBTC_LAUNCHED(ctx);
   }
+  // the streamed kernel finds block b's column offsets at co (BlockDesc.co)
+  for (uint32_t b = 0; b < nb; ++b) plan->blocks[b].co = plan->co_off[b];
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaStreamSynchronize(st));   // dco / dcuts die with this scope
   return len;
 }
 
-void colptr_expand(cudaStream_t st, const uint32_t* colptr, uint32_t ncols, uint32_t* ccv) {
-  if (!ncols) return;
-  const uint32_t grid = std::min<uint32_t>((ncols + 31) / 32, 4096u);
-  k_col_expand<<<grid, 32, 0, st>>>(colptr, ncols, ccv);
-  BBTC_CUDA(cudaGetLastError());
+void colptr_expand_all(bbtc_ctx* ctx, bbtc_plan* plan) {
+  const uint32_t nb = (uint32_t)plan->blocks.size();
+  if (!nb || !plan->m) return;
+  uint32_t maxc = 1;
+  for (auto& B : plan->blocks) maxc = std::max(maxc, B.nc);
+  dim3 grid(std::max(1u, std::min((maxc + 255) / 256, 256u)), std::min(nb, 16384u));
+  k_col_expand_all<<<grid, kThreads, 0, ctx->stream>>>(plan->d_colptr.p, plan->d_blocks.p, nb, plan->ccv.p);
+  BBTC_LAUNCHED(ctx);
 }
 
 // a3, automatic p: the smallest p whose largest task

@@ -26,7 +26,22 @@ def count_distributed(plan, counts, group=None):
     else:
         rank, world = 0, 1
     plan.count_async(counts, rank, world)
+    _after_ctx_stream(plan.ctx, counts)
     return reduce_counts(counts, group)
+
+
+def _after_ctx_stream(ctx, counts):
+    """Make torch's current stream (the one NCCL/gloo order the collective after) wait
+    for the count enqueued on the context's stream; a no-op when they are the same."""
+    if not getattr(counts, "is_cuda", False):
+        return
+    import torch
+    cur = torch.cuda.current_stream(counts.device)
+    h = ctx.stream
+    if h and h != cur.cuda_stream:
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(h, device=counts.device))
+        cur.wait_event(ev)
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:

@@ -19,6 +19,11 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "rmat16"
+    # the steps partition the rows: together they are one full count (nothing extrapolated)
+    import inputs
+    import oracle
+    s, dd = inputs.rmat(16, 16, 1)
+    assert d["triangles"] == oracle.OracleGraph(s, dd, 1 << 16).count(1)[0]
 
 
 def test_reference_arm_nonzero_rank_is_silent():

@@ -60,3 +60,16 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(bb.BBTCError) as ei:
         bb.Context(0)
     assert ei.value.code == -6  # BBTC_ECUDA
+
+
+def test_edge_ids_that_would_wrap_are_refused():
+    """Non-u32 id arrays are range-checked before the cast: 2^32+5 or -2 must not
+    silently become another vertex id."""
+    from paper_2009_12457_b200 import _ptr
+    ok = _ptr(np.array([0, 5, 0xFFFFFFFE], np.int64), np.uint32)
+    assert ok[1] == 3 and list(ok[3]) == [0, 5, 0xFFFFFFFE]
+    for bad in (np.array([1, 2**32 + 5], np.int64), np.array([3, -2], np.int64),
+                np.array([0xFFFFFFFF], np.uint64), np.array([1.5]), ):
+        with pytest.raises(OverflowError):
+            _ptr(bad, np.uint32)
+    assert _ptr(np.zeros(0, np.int64), np.uint32)[1] == 0
