@@ -229,7 +229,8 @@ __device__ __forceinline__ uint32_t col_of(const uint32_t* __restrict__ cp, uint
       const uint32_t t = __shfl_sync(kFull, w, pos + st - 1);
       if (t <= x) pos += st;
     }
-    if (pos == 31 && __shfl_sync(kFull, w, 31) <= x) pos = 32;
+    const uint32_t w31 = __shfl_sync(kFull, w, 31);   // (every lane: a warp-wide shuffle)
+    if (pos == 31 && w31 <= x) pos = 32;
     if (need && pos < 32) {
       v = c + pos;
       need = false;
