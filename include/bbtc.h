@@ -285,6 +285,80 @@ BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan);
 /* Drops the device copies made by bbtc_stage / streaming counts. */
 BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan);
 
+/* ------------------------------------------- multi-GPU sharded build (§8(e))
+ * One process per GPU, rank r of `world`, each starting from its own share of the
+ * raw edges.  The caller moves buffers between ranks (torch.distributed over NCCL:
+ * two all-to-alls, two all-reduces and point-to-point block transfers) between these
+ * per-rank device steps; see paper_2009_12457_b200/dist.py and DESIGN.md §9.  Tasks
+ * are independent and the result is the sum of per-task counts; the
+ * paper distributes tasks over GPUs in a ready queue — here a
+ * deterministic LPT with block affinity (bbtc_shard_assign) fixes every rank's tasks.
+ * All device arrays are on the context's device; all calls are stream-ordered on it
+ * and return after the host-visible outputs are written.
+ *
+ * a1 sharded: canonicalise this rank's n_edges raw pairs (mem: BBTC_MEM_HOST = the
+ * share crosses PCIe here, or BBTC_MEM_DEVICE), drop self-loops, sort, unique, and
+ * group the unique keys by destination rank (a hash of the smaller id, so every copy
+ * of an edge from any rank meets at one rank).  d_keys_out: DEVICE uint64[n_edges],
+ * receives send_counts[0] keys for rank 0, then rank 1's, … as (min << 32 | max).
+ * send_counts: HOST uint64[world].  *max_id_plus1: 1 + the largest raw id (0 if none).
+ * n_hint: a lower bound for n (narrows sort keys; any value is correct). */
+BBTC_API bbtc_status bbtc_shard_canon(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t n_edges,
+                                      int mem, uint32_t n_hint, uint32_t world, uint64_t* d_keys_out,
+                                      uint64_t* send_counts, uint32_t* max_id_plus1);
+/* a1-a2 sharded: the keys this rank received (every copy of its edges, from all ranks)
+ * are sorted and de-duplicated into a graph shard; d_deg: DEVICE uint32[n] receives
+ * this shard's partial full degrees (sum them over ranks).  n = the global vertex
+ * count (max of n_hint and every rank's max_id_plus1). */
+BBTC_API bbtc_status bbtc_shard_graph(bbtc_ctx* ctx, const uint64_t* d_keys, uint64_t n_keys, uint32_t n,
+                                      uint32_t* d_deg, bbtc_graph** out);
+/* a2 sharded: with the global degrees d_deg (DEVICE uint32[n], summed over ranks) and
+ * the global edge count, rank every vertex by (degree, id) (R2) and orient
+ * the shard's edges.  Errors: BBTC_ESTATE if g is not an unranked shard. */
+BBTC_API bbtc_status bbtc_shard_rank(bbtc_ctx* ctx, bbtc_graph* g, const uint32_t* d_deg, uint64_t m_total);
+/* a3 sharded: cuts (user cuts, or the default rule over the global degrees) and this
+ * shard's edge count of every block: d_block_nnz DEVICE uint64[p(p+1)/2] (block order
+ * b = j(j+1)/2 + i; sum over ranks), cuts_out HOST uint32[p+1], *p_eff = p after
+ * clamping (p > n -> n). */
+BBTC_API bbtc_status bbtc_shard_block_sizes(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                            uint64_t* d_block_nnz, uint32_t* cuts_out, uint32_t* p_eff);
+/* a5 + the multi-GPU scheduler (host only, deterministic): from the global block sizes,
+ * task_rank[idx] (HOST uint32[n_tasks], Alg. 4 order) = the rank counting task idx
+ * (LPT on the per-edge cost estimate with block affinity), and
+ * block_rank[b] (HOST uint32[p(p+1)/2]) = the rank that builds block b and forwards it
+ * to every other rank whose tasks read it. */
+BBTC_API bbtc_status bbtc_shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* block_nnz, uint32_t world,
+                                       uint32_t* task_rank, uint32_t* block_rank);
+/* a4 sharded, step 1: this shard's oriented edges grouped by the owner of their block:
+ * d_out DEVICE uint64[m of the shard] (ru << 32 | rw), send_counts HOST uint64[world]. */
+BBTC_API bbtc_status bbtc_shard_by_block(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                         const uint32_t* block_rank, uint32_t world, uint64_t* d_out,
+                                         uint64_t* send_counts);
+/* a4 sharded, step 2: rank `rank`'s plan in the GLOBAL block layout (block_nnz, the
+ * summed sizes): the blocks it owns are built from d_okeys (every edge of those blocks,
+ * as received), the others are allocated and filled by the caller through
+ * bbtc_plan_block_ptrs.  The plan holds only the tasks with task_rank[idx] == rank;
+ * bbtc_count_async(ctx, plan, rank, world, …) counts them.  `like` = this rank's
+ * ranked shard (vertex count, isolated prefix).  Errors: BBTC_EINVAL when a block
+ * arrives incomplete. */
+BBTC_API bbtc_status bbtc_plan_create_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* d_okeys,
+                                            uint64_t n_okeys, uint32_t p, const uint32_t* cuts,
+                                            const uint64_t* block_nnz, const uint32_t* task_rank, uint32_t rank,
+                                            uint32_t world, uint32_t flags, bbtc_plan** out);
+/* Device spans of block b of a resident plan: its n_edge_arrays per-edge arrays (cols,
+ * then the walk order: ccu, ccv for column-major plans, rows for row-major) of nnz
+ * words each, and its rowptr_len block-local row offsets.  For moving blocks between
+ * ranks (the spans are the plan's own memory; valid while the plan lives). */
+typedef struct {
+  uint32_t* edge[3];
+  uint32_t n_edge_arrays;
+  uint32_t reserved;
+  uint64_t nnz;
+  uint32_t* rowptr;
+  uint64_t rowptr_len;
+} bbtc_block_ptrs;
+BBTC_API bbtc_status bbtc_plan_block_ptrs(const bbtc_plan* plan, uint32_t b, bbtc_block_ptrs* out);
+
 /* Number of kernels this library launched on the context since creation. */
 BBTC_API uint64_t bbtc_ctx_launches(const bbtc_ctx* ctx);
 BBTC_API const char* bbtc_last_error(void);

@@ -49,6 +49,12 @@ int bbtcgen_gnp(uint32_t n, double q, uint64_t seed, uint32_t* src, uint32_t* ds
 /* Uniform random pairs in [0,n)^2 (may include self-loops and duplicates). */
 int bbtcgen_uniform_pairs(uint32_t n, uint64_t count, uint64_t seed, uint32_t* src, uint32_t* dst);
 
+/* Samples [start, start + count) of the same sequences (src/dst hold count entries):
+ * a rank generates its shard of the raw edge list without the rest. */
+int bbtcgen_rmat_range(uint32_t scale, uint32_t edgefactor, double a, double b, double c, uint64_t seed,
+                       uint64_t start, uint64_t count, uint32_t* src, uint32_t* dst, int threads);
+int bbtcgen_chunglu_range(uint32_t n, uint64_t m, double gamma, double dmax, uint64_t seed, uint64_t start,
+                          uint64_t count, uint32_t* src, uint32_t* dst, double* dmin_out, int threads);
 const char* bbtcgen_last_error(void);
 
 #ifdef __cplusplus

@@ -42,6 +42,12 @@ def _load():
         lib.bbtcgen_gnp.argtypes = [ctypes.c_uint32, ctypes.c_double, ctypes.c_uint64, _u32p, _u32p,
                                     ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
         lib.bbtcgen_uniform_pairs.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u32p, _u32p]
+        lib.bbtcgen_rmat_range.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                           _u32p, _u32p, ctypes.c_int]
+        lib.bbtcgen_chunglu_range.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _u32p, _u32p,
+                                              ctypes.POINTER(ctypes.c_double), ctypes.c_int]
         lib.bbtcgen_last_error.restype = ctypes.c_char_p
         _lib = lib
     return _lib
@@ -139,6 +145,32 @@ class Config:
         if self.kind == "rmat":
             return 16 << self.scale
         return self.m
+
+    def shard(self, rank: int, world: int) -> tuple:
+        """[start, end) of rank's contiguous share of the raw samples."""
+        E = self.n_samples
+        return E * rank // world, E * (rank + 1) // world
+
+    def generate_range(self, start: int, count: int, seed: int = 1, out=None, threads=0):
+        """Raw samples [start, start+count) of this config (a rank's shard)."""
+        if self.kind == "karate":
+            s, d = karate()
+            s, d = s[start:start + count].copy(), d[start:start + count].copy()
+            if out is not None:
+                out[0][:count] = s
+                out[1][:count] = d
+                return out[0][:count], out[1][:count]
+            return s, d
+        s, d = _out(count, out)
+        L = _load()
+        if self.kind == "rmat":
+            _check(L.bbtcgen_rmat_range(self.scale, 16, 0.57, 0.19, 0.19, seed, start, count, _ptr(s), _ptr(d),
+                                        threads))
+        else:
+            dmin = ctypes.c_double()
+            _check(L.bbtcgen_chunglu_range(self.n, self.m, self.gamma, self.dmax, seed, start, count, _ptr(s),
+                                           _ptr(d), ctypes.byref(dmin), threads))
+        return s, d
 
     def generate(self, seed: int = 1, out=None, threads=0):
         """Raw (src, dst) uint32 samples for this config."""

@@ -32,16 +32,21 @@ static inline uint64_t below(uint64_t h, uint64_t n) {                         /
 }
 static inline int nthreads(int t) { return t > 0 ? t : omp_get_max_threads(); }
 
-extern "C" int bbtcgen_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
-                            uint32_t* src, uint32_t* dst, int threads) {
+// Samples [start, start + count) of the R-MAT sequence (src/dst hold count entries):
+// each sample is a pure function of (seed, e), so ranks can generate their shards.
+extern "C" int bbtcgen_rmat_range(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                                  uint64_t start, uint64_t count, uint32_t* src, uint32_t* dst, int threads) {
   if (scale == 0 || scale > 32) return fail("rmat: scale must be in 1..32");
   double d = 1.0 - a - b - c;
   if (a <= 0 || b < 0 || c < 0 || d < 0) return fail("rmat: need a>0, b,c,d>=0, a+b+c<=1");
   if (!src || !dst) return fail("rmat: null output");
   const uint64_t ns = (uint64_t)ef << scale;
+  if (start > ns || count > ns - start) return fail("rmat: sample range past the end");
   const double ab = a + b, a_norm = a / ab, c_norm = c / (c + d);
+  src -= start;
+  dst -= start;
 #pragma omp parallel for schedule(static) num_threads(nthreads(threads))
-  for (int64_t e = 0; e < (int64_t)ns; ++e) {
+  for (int64_t e = (int64_t)start; e < (int64_t)(start + count); ++e) {
     uint64_t s = 0, t = 0;
     for (uint32_t l = 0; l < scale; ++l) {
       uint64_t ctr = (((uint64_t)e << 6) | l) << 1;
@@ -56,6 +61,12 @@ extern "C" int bbtcgen_rmat(uint32_t scale, uint32_t ef, double a, double b, dou
   return 0;
 }
 
+extern "C" int bbtcgen_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                            uint32_t* src, uint32_t* dst, int threads) {
+  if (scale == 0 || scale > 32) return fail("rmat: scale must be in 1..32");
+  return bbtcgen_rmat_range(scale, ef, a, b, c, seed, 0, (uint64_t)ef << scale, src, dst, threads);
+}
+
 // Mean of a Pareto(gamma) truncated to [lo, hi].
 static double trunc_pareto_mean(double g, double lo, double hi) {
   if (std::fabs(g - 2.0) < 1e-12) return std::log(hi / lo) / (1.0 / lo - 1.0 / hi);
@@ -63,8 +74,9 @@ static double trunc_pareto_mean(double g, double lo, double hi) {
          (std::pow(lo, 1.0 - g) - std::pow(hi, 1.0 - g));
 }
 
-extern "C" int bbtcgen_chunglu(uint32_t n, uint64_t m, double g, double dmax, uint64_t seed,
-                               uint32_t* src, uint32_t* dst, double* dmin_out, int threads) {
+extern "C" int bbtcgen_chunglu_range(uint32_t n, uint64_t m, double g, double dmax, uint64_t seed, uint64_t start,
+                                     uint64_t count, uint32_t* src, uint32_t* dst, double* dmin_out, int threads) {
+  if (start > m || count > m - start) return fail("chunglu: sample range past the end");
   if (n < 2) return fail("chunglu: n must be >= 2");
   if (!(g > 1.0)) return fail("chunglu: gamma must be > 1");
   const double target = 2.0 * (double)m / (double)n;
@@ -116,8 +128,10 @@ extern "C" int bbtcgen_chunglu(uint32_t n, uint64_t m, double g, double dmax, ui
     uint32_t j = (uint32_t)below(bbtcgen_u64(pseed, i), (uint64_t)i + 1);
     uint32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
   }
+  src -= start;
+  dst -= start;
 #pragma omp parallel for schedule(static) num_threads(nthreads(threads))
-  for (int64_t e = 0; e < (int64_t)m; ++e) {
+  for (int64_t e = (int64_t)start; e < (int64_t)(start + count); ++e) {
     uint32_t ends[2];
     for (int side = 0; side < 2; ++side) {
       uint64_t ctr = (((uint64_t)e << 1) | side) << 1;
@@ -128,6 +142,11 @@ extern "C" int bbtcgen_chunglu(uint32_t n, uint64_t m, double g, double dmax, ui
     dst[e] = perm[ends[1]];
   }
   return 0;
+}
+
+extern "C" int bbtcgen_chunglu(uint32_t n, uint64_t m, double g, double dmax, uint64_t seed,
+                               uint32_t* src, uint32_t* dst, double* dmin_out, int threads) {
+  return bbtcgen_chunglu_range(n, m, g, dmax, seed, 0, m, src, dst, dmin_out, threads);
 }
 
 extern "C" int bbtcgen_gnp(uint32_t n, double q, uint64_t seed, uint32_t* src, uint32_t* dst,

@@ -68,6 +68,11 @@ class bbtc_timing(ctypes.Structure):
                 ("h2d_bytes", c_u64), ("launches", c_u64), ("t_dense_ms", ctypes.c_double)]
 
 
+class bbtc_block_ptrs(ctypes.Structure):
+    _fields_ = [("edge", _vp * 3), ("n_edge_arrays", c_u32), ("reserved", c_u32), ("nnz", c_u64),
+                ("rowptr", _vp), ("rowptr_len", c_u64)]
+
+
 def _sig(name, res, *args):
     f = getattr(lib, name)
     f.restype = res
@@ -104,6 +109,16 @@ bbtc_count_async = _sig("bbtc_count_async", _st, _vp, _vp, c_u32, c_u32, _vp)
 bbtc_count = _sig("bbtc_count", _st, _vp, _vp, c_u32, c_u32, c_u32, _u64p, _u64p, ctypes.POINTER(bbtc_timing))
 bbtc_stage = _sig("bbtc_stage", _st, _vp, _vp)
 bbtc_unstage = _sig("bbtc_unstage", _st, _vp, _vp)
+bbtc_shard_canon = _sig("bbtc_shard_canon", _st, _vp, _vp, _vp, c_u64, ctypes.c_int, c_u32, c_u32, _vp, _u64p,
+                        _u32p)
+bbtc_shard_graph = _sig("bbtc_shard_graph", _st, _vp, _vp, c_u64, c_u32, _vp, _pp)
+bbtc_shard_rank = _sig("bbtc_shard_rank", _st, _vp, _vp, _vp, c_u64)
+bbtc_shard_block_sizes = _sig("bbtc_shard_block_sizes", _st, _vp, _vp, c_u32, _u32p, _vp, _u32p, _u32p)
+bbtc_shard_assign = _sig("bbtc_shard_assign", _st, c_u32, _u32p, _u64p, c_u32, _u32p, _u32p)
+bbtc_shard_by_block = _sig("bbtc_shard_by_block", _st, _vp, _vp, c_u32, _u32p, _u32p, c_u32, _vp, _u64p)
+bbtc_plan_create_shard = _sig("bbtc_plan_create_shard", _st, _vp, _vp, _vp, c_u64, c_u32, _u32p, _u64p, _u32p,
+                              c_u32, c_u32, c_u32, _pp)
+bbtc_plan_block_ptrs = _sig("bbtc_plan_block_ptrs", _st, _vp, c_u32, ctypes.POINTER(bbtc_block_ptrs))
 bbtc_last_error = _sig("bbtc_last_error", ctypes.c_char_p)
 bbtc_version = _sig("bbtc_version", ctypes.c_char_p)
 

@@ -152,12 +152,17 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     const uint32_t rows = plan->cuts[B.i + 1] - plan->cuts[B.i];
     return rows ? (double)B.nnz / rows : 0.0;
   };
+  // §8(e) shard plans keep only their rank's tasks (and size work items for them).
+  auto mine = [&](uint32_t i, uint32_t j, uint32_t k) {
+    return plan->task_rank.empty() || plan->task_rank[task_index(p, i, j, k)] == plan->shard_rank;
+  };
   double work_total = 0;
   for (uint32_t k = 0; k < p; ++k)
     for (uint32_t j = 0; j <= k; ++j)
       for (uint32_t i = 0; i <= j; ++i)
-        work_total += (double)plan->blocks[block_id(i, j)].nnz *
-                      (8.0 + delta(block_id(i, k)) + delta(block_id(j, k)));
+        if (mine(i, j, k))
+          work_total += (double)plan->blocks[block_id(i, j)].nnz *
+                        (8.0 + delta(block_id(i, k)) + delta(block_id(j, k)));
   // ~384 items per warp slot of a full B200 (148 SMs x 40 warps); BBTC_ITEMS_PER_SLOT
   // overrides.  The estimate is uniform over a task's edges while the real cost is not
   // (hub columns: long runs x long probe lists), so fine items balance the tail:
@@ -235,7 +240,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   };
   {
     std::vector<std::array<uint32_t, 3>> sparse, dense;
-    for (const auto& t : order) (is_dense(t[0], t[1], t[2]) ? dense : sparse).push_back(t);
+    for (const auto& t : order)
+      if (mine(t[0], t[1], t[2])) (is_dense(t[0], t[1], t[2]) ? dense : sparse).push_back(t);
     plan->dense_task_lo = (uint32_t)sparse.size();
     order = sparse;
     order.insert(order.end(), dense.begin(), dense.end());
@@ -249,6 +255,7 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         T.ik = block_id(i, k);
         T.jk = block_id(j, k);
         T.idx = (uint32_t)task_index(p, i, j, k);
+        T.icol = 0;
         if (plan->tasks.size() == plan->dense_task_lo) plan->dense_item_lo = plan->item_start.back();
         T.pad = plan->tasks.size() >= plan->dense_task_lo ? plan->dense_s[k] : 0;
         {
@@ -274,6 +281,14 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     }
   }
   if (plan->dense_task_lo >= plan->tasks.size()) plan->dense_item_lo = plan->item_start.back();
+  {   // item_col bases in canonical task order: independent of the execution order, so
+      // streaming / out-of-core re-orderings keep using one item_col array
+    std::vector<uint64_t> base(n_tasks(p) + 1, 0);
+    for (size_t t = 0; t < plan->tasks.size(); ++t)
+      base[plan->tasks[t].idx + 1] = plan->item_start[t + 1] - plan->item_start[t];
+    for (size_t x = 0; x + 1 < base.size(); ++x) base[x + 1] += base[x];
+    for (auto& T : plan->tasks) T.icol = (uint32_t)base[T.idx];
+  }
   {   // compulsory bytes of both kernels (roofline denominators)
     std::vector<char> seen(plan->blocks.size(), 0), seen_d(plan->blocks.size(), 0);
     uint64_t lb = 0, db = 0;
@@ -306,6 +321,77 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
   // The host vectors are read by the async copies above: make them complete
   // before the caller can mutate the plan.
   BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---- §8(e) scheduler: tasks -> ranks, blocks -> owners --------------------------------
+// Deterministic on every rank (same inputs: cuts and the all-reduced block sizes).
+// Tasks in decreasing estimated work (the ExecTime-style per-edge cost of plan_tasks,
+// P:658-667; ties by canonical index) go to a rank by LPT with block affinity: among
+// the ranks whose load would stay within 2% above the ideal share (or the least-loaded
+// rank's load plus the task), the one already holding most of the task's block bytes,
+// so tasks sharing blocks gather on few ranks and fewer blocks cross NVLink.  A block's
+// owner (the rank that builds it and forwards it) is the needer holding the fewest
+// owned bytes so far, visiting blocks largest first; unneeded blocks round-robin.
+void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32_t world, uint32_t* task_rank,
+                  uint32_t* block_rank) {
+  const uint32_t nb = p * (p + 1) / 2;
+  const uint64_t nt = n_tasks(p);
+  auto rows = [&](uint32_t i) { return (uint64_t)(cuts[i + 1] - cuts[i]); };
+  auto delta = [&](uint32_t i, uint32_t j) {
+    const uint64_t r = rows(i);
+    return r ? (double)bnnz[block_id(i, j)] / (double)r : 0.0;
+  };
+  auto bbytes = [&](uint32_t b, uint32_t i) { return 12.0 * (double)bnnz[b] + 4.0 * (double)(rows(i) + 1); };
+  struct T { double w; uint64_t idx; uint32_t i, j, k; };
+  std::vector<T> ts;
+  ts.reserve(nt);
+  double total = 0;
+  for (uint32_t i = 0; i < p; ++i)
+    for (uint32_t j = i; j < p; ++j)
+      for (uint32_t k = j; k < p; ++k) {
+        const double w = (double)bnnz[block_id(i, j)] * (8.0 + delta(i, k) + delta(j, k));
+        ts.push_back({w, task_index(p, i, j, k), i, j, k});
+        total += w;
+      }
+  std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.w > b.w || (a.w == b.w && a.idx < b.idx); });
+  std::vector<double> load(world, 0.0);
+  std::vector<std::vector<char>> has(world, std::vector<char>(nb, 0));
+  const double share = total / world * 1.02;
+  for (const T& t : ts) {
+    const uint32_t bl[3] = {block_id(t.i, t.j), block_id(t.i, t.k), block_id(t.j, t.k)};
+    const uint32_t bi[3] = {t.i, t.i, t.j};
+    const double lmin = *std::min_element(load.begin(), load.end());
+    const double cap = std::max(share, lmin + t.w);
+    int best = -1;
+    double best_aff = -1;
+    for (uint32_t r = 0; r < world; ++r) {
+      if (load[r] + t.w > cap + 1e-9) continue;
+      double aff = 0;
+      for (int x = 0; x < 3; ++x)
+        if (has[r][bl[x]] && (x == 0 || bl[x] != bl[0]) && (x < 2 || bl[x] != bl[1])) aff += bbytes(bl[x], bi[x]);
+      if (aff > best_aff || (aff == best_aff && load[r] < load[best])) {
+        best = (int)r;
+        best_aff = aff;
+      }
+    }
+    task_rank[t.idx] = (uint32_t)best;
+    load[best] += t.w;
+    for (int x = 0; x < 3; ++x) has[best][bl[x]] = 1;
+  }
+  // owners
+  std::vector<uint32_t> border(nb);
+  for (uint32_t b = 0; b < nb; ++b) border[b] = b;
+  std::stable_sort(border.begin(), border.end(), [&](uint32_t a, uint32_t b) { return bnnz[a] > bnnz[b]; });
+  std::vector<double> owned(world, 0.0);
+  uint32_t rr = 0;
+  for (uint32_t b : border) {
+    int best = -1;
+    for (uint32_t r = 0; r < world; ++r)
+      if (has[r][b] && (best < 0 || owned[r] < owned[best])) best = (int)r;
+    if (best < 0) best = (int)(rr++ % world);
+    block_rank[b] = (uint32_t)best;
+    owned[best] += (double)bnnz[b];
+  }
 }
 
 // ---- a6: the block streamer -------------------------------------------------------
@@ -965,7 +1051,133 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
     if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
     if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident: call bbtc_stage or bbtc_count");
     count_zero(ctx, plan, d_counts);
+    if (plan->shard_world) {   // a shard plan holds exactly its rank's tasks
+      if (rank != plan->shard_rank || world != plan->shard_world)
+        raise(BBTC_EINVAL, "a shard plan counts only its own rank of its own world");
+      rank = 0;
+      world = 1;
+    }
     count_resident(ctx, const_cast<bbtc_plan*>(plan), rank, world, d_counts);
+  });
+}
+
+// ---- §8(e) sharded build ------------------------------------------------------------
+BBTC_API bbtc_status bbtc_shard_canon(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t n_edges,
+                                      int mem, uint32_t n_hint, uint32_t world, uint64_t* d_keys_out,
+                                      uint64_t* send_counts, uint32_t* max_id_plus1) {
+  return guard([&] {
+    if (!ctx || !send_counts || !max_id_plus1 || (n_edges && (!src || !dst || !d_keys_out)))
+      raise(BBTC_EINVAL, "NULL argument");
+    if (world == 0) raise(BBTC_EINVAL, "world must be >= 1");
+    if (mem != BBTC_MEM_HOST && mem != BBTC_MEM_DEVICE) raise(BBTC_EINVAL, "mem must be BBTC_MEM_HOST or _DEVICE");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    shard_canon(ctx, src, dst, n_edges, mem, n_hint, world, d_keys_out, send_counts, max_id_plus1);
+    if (*max_id_plus1 == 0 && n_edges) raise(BBTC_ERANGE, "vertex id 0xFFFFFFFF is reserved");
+  });
+}
+
+BBTC_API bbtc_status bbtc_shard_graph(bbtc_ctx* ctx, const uint64_t* d_keys, uint64_t n_keys, uint32_t n,
+                                      uint32_t* d_deg, bbtc_graph** out) {
+  return guard([&] {
+    if (!ctx || !out || !d_deg || (n_keys && !d_keys)) raise(BBTC_EINVAL, "NULL argument");
+    if (n == 0xFFFFFFFFu) raise(BBTC_ERANGE, "n must be < 2^32-1");
+    *out = nullptr;
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new bbtc_graph();
+    g->ctx = ctx;
+    try {
+      shard_graph(ctx, d_keys, n_keys, n, d_deg, g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+BBTC_API bbtc_status bbtc_shard_rank(bbtc_ctx* ctx, bbtc_graph* g, const uint32_t* d_deg, uint64_t m_total) {
+  return guard([&] {
+    if (!ctx || !g || !d_deg) raise(BBTC_EINVAL, "NULL argument");
+    if (!g->ckeys.p && g->m) raise(BBTC_ESTATE, "graph is not an unranked shard (bbtc_shard_graph)");
+    if (m_total < g->m) raise(BBTC_EINVAL, "m_total is below this shard's edge count");
+    if (m_total >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    shard_rank(ctx, g, d_deg, m_total);
+  });
+}
+
+BBTC_API bbtc_status bbtc_shard_block_sizes(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                            uint64_t* d_block_nnz, uint32_t* cuts_out, uint32_t* p_eff) {
+  return guard([&] {
+    if (!ctx || !g || !d_block_nnz || !cuts_out || !p_eff) raise(BBTC_EINVAL, "NULL argument");
+    if (p == 0) raise(BBTC_EINVAL, "p must be >= 1");
+    if (p > 4096) raise(BBTC_ERANGE, "p > 4096");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    *p_eff = shard_blocks_hist(ctx, g, p, cuts, d_block_nnz, cuts_out);
+  });
+}
+
+BBTC_API bbtc_status bbtc_shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* block_nnz, uint32_t world,
+                                       uint32_t* task_rank, uint32_t* block_rank) {
+  return guard([&] {
+    if (!cuts || !block_nnz || !task_rank || !block_rank) raise(BBTC_EINVAL, "NULL argument");
+    if (p == 0 || world == 0) raise(BBTC_EINVAL, "need p >= 1 and world >= 1");
+    for (uint32_t i = 0; i < p; ++i)
+      if (cuts[i] > cuts[i + 1]) raise(BBTC_EINVAL, "cuts must be non-decreasing");
+    shard_assign(p, cuts, block_nnz, world, task_rank, block_rank);
+  });
+}
+
+BBTC_API bbtc_status bbtc_shard_by_block(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts,
+                                         const uint32_t* block_rank, uint32_t world, uint64_t* d_out,
+                                         uint64_t* send_counts) {
+  return guard([&] {
+    if (!ctx || !g || !cuts || !block_rank || !send_counts || (g->m && !d_out)) raise(BBTC_EINVAL, "NULL argument");
+    if (world == 0 || p == 0) raise(BBTC_EINVAL, "need p >= 1 and world >= 1");
+    const uint32_t nb = p * (p + 1) / 2;
+    for (uint32_t b = 0; b < nb; ++b)
+      if (block_rank[b] >= world) raise(BBTC_EINVAL, "block owner >= world");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    shard_by_block(ctx, g, p, cuts, block_rank, world, d_out, send_counts);
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_create_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* d_okeys,
+                                            uint64_t n_okeys, uint32_t p, const uint32_t* cuts,
+                                            const uint64_t* block_nnz, const uint32_t* task_rank, uint32_t rank,
+                                            uint32_t world, uint32_t flags, bbtc_plan** out) {
+  return guard([&] {
+    if (!ctx || !like || !cuts || !block_nnz || !task_rank || !out || (n_okeys && !d_okeys))
+      raise(BBTC_EINVAL, "NULL argument");
+    if (p == 0 || world == 0 || rank >= world) raise(BBTC_EINVAL, "need p >= 1 and rank < world");
+    *out = nullptr;
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    auto* plan = new bbtc_plan();
+    plan->ctx = ctx;
+    try {
+      plan_build_shard(ctx, like, d_okeys, n_okeys, p, cuts, block_nnz, task_rank, rank, world, flags, plan);
+    } catch (...) {
+      bbtc_plan_free(plan);
+      throw;
+    }
+    *out = plan;
+  });
+}
+
+BBTC_API bbtc_status bbtc_plan_block_ptrs(const bbtc_plan* plan, uint32_t b, bbtc_block_ptrs* out) {
+  return guard([&] {
+    if (!plan || !out) raise(BBTC_EINVAL, "NULL argument");
+    if (b >= plan->blocks.size()) raise(BBTC_EINVAL, "block id >= p(p+1)/2");
+    if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident");
+    bbtc_plan* pl = const_cast<bbtc_plan*>(plan);
+    const BlockDesc& B = plan->blocks[b];
+    auto arenas = pl->edge_arenas();
+    std::memset(out, 0, sizeof(*out));
+    out->n_edge_arrays = (uint32_t)arenas.size();
+    for (size_t x = 0; x < arenas.size(); ++x) out->edge[x] = arenas[x].dev->p + B.e0;
+    out->nnz = B.nnz;
+    out->rowptr = pl->rowptr.p + B.ro;
+    out->rowptr_len = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
   });
 }
 
@@ -976,6 +1188,12 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
     if (!ctx || !cplan || !total) raise(BBTC_EINVAL, "NULL argument");
     if (world == 0 || rank >= world) raise(BBTC_EINVAL, "need rank < world");
     bbtc_plan* plan = const_cast<bbtc_plan*>(cplan);   // residency state only
+    if (plan->shard_world) {   // a shard plan holds exactly its rank's tasks
+      if (rank != plan->shard_rank || world != plan->shard_world)
+        raise(BBTC_EINVAL, "a shard plan counts only its own rank of its own world");
+      rank = 0;
+      world = 1;
+    }
     BBTC_CUDA(cudaSetDevice(ctx->device));
     const auto t0 = std::chrono::steady_clock::now();
     const uint64_t l0 = ctx->launches;
@@ -1043,6 +1261,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       full.rowptr = plan->rowptr.p;
       full.blocks = plan->d_blocks.p;
       full.colptr = plan->streams_colptr() ? plan->d_colptr.p : nullptr;
+      full.item_col = plan->d_item_col.p;
       count_launch(ctx, plan, rank, world, d_counts.p, 0, plan->dense_item_lo, plan->d_ready.p, epoch, &full,
                    greedy ? plan->d_s_tasks.p : nullptr, greedy ? plan->d_s_item_start.p : nullptr);
       // the count stream must not run past copies it did not wait for
@@ -1223,6 +1442,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         ar.rowptr = cache_rp.p;
         ar.blocks = tables.back().p;
         ar.colptr = cpf ? cache_rp.p : nullptr;
+        ar.item_col = plan->d_item_col.p;
         count_launch(ctx, plan, rank, world, d_counts.p, plan->item_start[t0w], plan->item_start[t1w],
                      plan->d_ready.p, epoch, &ar);
         ev_done.emplace_back();

@@ -237,7 +237,14 @@ __device__ __forceinline__ uint32_t col_of(const uint32_t* __restrict__ cp, uint
     }
     const uint32_t un = __ballot_sync(kFull, need);
     if (!un) break;
-    c = col_search(cp, c + 32, nc, __shfl_sync(kFull, x, __ffs(un) - 1), lane);
+    // Past the window: gallop — lane l probes column c + 32*2^l (one load per lane), the
+    // first probe past the first unresolved edge bounds a col_search over that octave.
+    const uint32_t xf = __shfl_sync(kFull, x, __ffs(un) - 1);
+    typedef unsigned long long u64;
+    const u64 at = min((u64)c + (32ull << lane), (u64)nc);
+    const uint32_t t = __popc(__ballot_sync(kFull, at < nc && cp[at] <= xf));   // >= 1: cp[c+32] <= xf
+    const uint32_t lo = (uint32_t)((u64)c + (32ull << (t - 1)));
+    c = col_search(cp, lo, (uint32_t)min((u64)c + (32ull << t), (u64)nc), xf, lane);
   }
   return v;
 }
@@ -255,7 +262,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
         unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch,
-        const uint32_t* __restrict__ colptr) {
+        const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ item_col) {
   static_assert(!kCP || kCol, "column offsets replace the column ids of a column-major walk");
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -305,7 +312,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     const uint32_t* rpP = rowptr + BP.ro;
     const uint32_t* cpb = kCP ? colptr + Bij.co : nullptr;   // G_ij's column offsets (kCP)
     uint32_t ccol = 0;                                        // a column with cpb[ccol] <= next edge
-    if constexpr (kCP) ccol = col_search(cpb, 0, Bij.nc, (uint32_t)(e_begin - Bij.e0), lane);
+    if constexpr (kCP) ccol = item_col[T.icol + (g - item_start[lo])];   // (k_item_cols, plan time)
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
@@ -690,12 +697,13 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
                          const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
                          unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t,
-                         const uint32_t*);
+                         const uint32_t*, const uint32_t*);
   // The bitmap variant only where some task's V_k is small enough (it costs the main
   // loop a few registers: friendster, whose parts are all large, measured 0.7% slower).
   bool bm = false;
   for (const TaskDesc& T : plan->tasks) bm = bm || T.bmw != 0;
   const bool cp = ar && ar->colptr && plan->colmajor;
+  if (cp && !ar->item_col) raise(BBTC_ESTATE, "column-offset walk without item start columns");
   const int variant = (hash ? 1 : 0) | (plan->colmajor ? 2 : 0) | (kBitmap && bm ? 4 : 0) | (cp ? 8 : 0);
   static const KernT kerns[16] = {
       k_count<false, false, false, false>, k_count<true, false, false, false>,
@@ -738,7 +746,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
       (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
-      (uint32_t)nt, ready, epoch, ar->colptr);
+      (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col);
   BBTC_LAUNCHED(ctx);
 }
 

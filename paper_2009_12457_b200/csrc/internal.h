@@ -115,6 +115,11 @@ struct bbtc_graph {
   bbtc::DevBuf<uint32_t> deg_sorted;  // full degrees in rank order (n)
   bbtc::DevBuf<uint32_t> rank;        // rank of each input id (n)
   bbtc::DevBuf<uint64_t> okeys;       // oriented edges (ru << 32 | rw), ru < rw, unsorted (m)
+  // §8(e) shards: m counts this rank's edges, m_total the whole graph's (default cuts
+  // use 2 m_total); ckeys = the shard's canonical keys (lo << cbw | hi) until ranked.
+  uint64_t m_total = 0;
+  int cbw = 32;
+  bbtc::DevBuf<uint64_t> ckeys;
 };
 
 // One upper-triangular block G_ij in the arena (column-major block order:
@@ -136,6 +141,7 @@ struct TaskDesc {
   uint32_t chunk;       // edges of G_ij per work item
   uint32_t pad;         // dense tasks: bit-row stride of V_k in words
   uint32_t bmw;         // words of a bitmap over V_k (power of two >= 4) if it fits a warp's table, else 0
+  uint32_t icol;        // first entry of this task's items in item_col (canonical task order)
 };
 
 struct bbtc_plan {
@@ -155,6 +161,7 @@ struct bbtc_plan {
   bbtc::DevBuf<uint32_t> rowptr;      // sum over blocks of |V_i|+1
   bbtc::DevBuf<uint32_t> ccu, ccv;    // m: column-major iteration order (u, v) of each block
   bbtc::DevBuf<uint32_t> d_colptr;    // streamed column-major plans: per block at co, |V_j|+1 local column offsets
+  bbtc::DevBuf<uint32_t> d_item_col;  // host plans: the column of every work item's first edge (at TaskDesc.icol)
   bool colmajor = true;               // kernel walks G_ij by column (ccu/ccv) vs by row (rows/cols)
   bbtc::DevBuf<BlockDesc> d_blocks;
   bbtc::DevBuf<TaskDesc> d_tasks;
@@ -195,6 +202,10 @@ struct bbtc_plan {
   bbtc::DevBuf<uint64_t> d_dense_off;
   // Streamed counts (a6): the sparse tasks in block-unlock order (greedy most work per
   // byte still to copy), so the kernel has work while later blocks are in flight.
+  // §8(e) shard plans: the tasks of rank shard_rank only (task_rank[canonical idx]),
+  // blocks at their global offsets; 0 = an ordinary plan.
+  std::vector<uint32_t> task_rank;
+  uint32_t shard_rank = 0, shard_world = 0;
   bool s_ready = false;
   std::vector<TaskDesc> s_tasks;
   std::vector<uint64_t> s_item_start;
@@ -234,6 +245,7 @@ struct DevArenas {
   const uint32_t* rowptr = nullptr;
   const BlockDesc* blocks = nullptr;
   const uint32_t* colptr = nullptr;   // column offsets (BlockDesc.co / nc) instead of it_v
+  const uint32_t* item_col = nullptr; // with colptr: each work item's start column (TaskDesc.icol)
 };
 void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
@@ -252,6 +264,20 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, bbtc::DevBuf<uint32_t>* ou
 void colptr_expand_all(bbtc_ctx* ctx, bbtc_plan* plan);
 void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                         uint64_t item_lo, uint64_t item_hi);
+// §8(e) sharded build (prep.cu)
+void shard_canon(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, int mem, uint32_t n_hint,
+                 uint32_t world, uint64_t* out, uint64_t* send_counts, uint32_t* max_id_plus1);
+void shard_graph(bbtc_ctx* ctx, const uint64_t* wire, uint64_t cnt, uint32_t n, uint32_t* d_deg, bbtc_graph* g);
+void shard_rank(bbtc_ctx* ctx, bbtc_graph* g, const uint32_t* d_deg, uint64_t m_total);
+uint32_t shard_blocks_hist(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts,
+                           uint64_t* d_bnnz, uint32_t* cuts_out);
+void shard_by_block(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts, const uint32_t* owner,
+                    uint32_t world, uint64_t* out, uint64_t* send_counts);
+void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* okeys, uint64_t cnt, uint32_t p,
+                      const uint32_t* cuts, const uint64_t* bnnz, const uint32_t* task_rank, uint32_t rank,
+                      uint32_t world, uint32_t flags, bbtc_plan* plan);
+void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32_t world, uint32_t* task_rank,
+                  uint32_t* block_rank);
 // capi.cpp (host)
 uint64_t n_tasks(uint32_t p);
 uint64_t task_index(uint32_t p, uint32_t i, uint32_t j, uint32_t k);

@@ -382,6 +382,31 @@ __global__ void k_col_local(const BlockDesc* __restrict__ blocks, const uint64_t
       colptr[co[b] + c] -= (uint32_t)B.e0;
   }
 }
+// The column of every work item's first edge (streamed column-major plans): items in
+// execution order, written at item_col[T.icol + item - item_start[t]].
+__global__ void k_item_cols(const TaskDesc* __restrict__ tasks, const uint64_t* __restrict__ item_start,
+                            uint32_t n_exec, uint64_t n_items, const BlockDesc* __restrict__ blocks,
+                            const uint32_t* __restrict__ colptr, const uint64_t* __restrict__ co,
+                            uint32_t* __restrict__ item_col) {
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n_items;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = n_exec - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const TaskDesc T = tasks[lo];
+    const uint64_t x = (g - item_start[lo]) * T.chunk;   // local offset of the item's first edge
+    const uint32_t* cp = colptr + co[T.ij];
+    uint32_t a = 0, b = blocks[T.ij].nc - 1;               // largest c with cp[c] <= x
+    while (a < b) {
+      const uint32_t mid = a + (b - a + 1) / 2;
+      if (cp[mid] <= x) a = mid; else b = mid - 1;
+    }
+    item_col[T.icol + (g - item_start[lo])] = a;
+  }
+}
+
 // ccv from the column offsets once a streamed count's copies have landed (context
 // stream, ordered after the count kernel): ccv[e0 + x] = c for every edge x of column
 // c of every block.  A warp per 32 columns, lanes over a column's edges.
@@ -427,6 +452,89 @@ __global__ void k_low_bits(const K* __restrict__ keys, uint64_t m, int cb, uint3
   const K mask = ((K)1 << cb) - 1;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
     out[e] = (uint32_t)(keys[e] & mask);
+}
+
+// ---- §8(e) sharded build: grouping keys by destination rank -----------------------
+// Owner rank of a canonical edge (lo << 32 | hi): a hash of its lower id, so every
+// instance of an edge (from any rank's raw shard) meets at one rank.
+__device__ __forceinline__ uint32_t key_owner(uint64_t lo, uint32_t world) {
+  return (uint32_t)(((lo * 0x9E3779B97F4A7C15ull) >> 32) % world);
+}
+// Owner rank of an oriented edge (ru << 32 | rw): the owner of its block (part ru, part rw).
+__device__ __forceinline__ uint32_t okey_owner(uint64_t k, const uint32_t* s_cuts, uint32_t p,
+                                               const uint32_t* s_owner) {
+  const uint32_t i = part_of(s_cuts, p, (uint32_t)(k >> 32)), j = part_of(s_cuts, p, (uint32_t)k);
+  return s_owner[j * (j + 1) / 2 + i];
+}
+// Counting pass + scatter pass over keys: dest[w] counts, then keys land in their
+// owner's range (order inside a range is arbitrary: receivers sort).  kind 0: canonical
+// keys by key_owner; kind 1: oriented keys by block owner (cuts/owner in shared memory).
+template <int kKind>
+__global__ void k_dest_count(const uint64_t* __restrict__ keys, uint64_t m, uint32_t world, int bw,
+                             const uint32_t* __restrict__ gcuts, uint32_t p, const uint32_t* __restrict__ gowner,
+                             unsigned long long* __restrict__ counts) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* s_cnt = sh;                 // world
+  uint32_t* s_cuts = sh + world;        // p + 1
+  uint32_t* s_owner = s_cuts + p + 1;   // p(p+1)/2
+  for (uint32_t x = threadIdx.x; x < world; x += blockDim.x) s_cnt[x] = 0;
+  if (kKind == 1) {
+    for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+    for (uint32_t x = threadIdx.x; x < p * (p + 1) / 2; x += blockDim.x) s_owner[x] = gowner[x];
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    const uint32_t w = kKind == 0 ? key_owner(k >> bw, world) : okey_owner(k, s_cuts, p, s_owner);
+    atomicAdd(&s_cnt[w], 1u);
+  }
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < world; x += blockDim.x)
+    if (s_cnt[x]) atomicAdd(&counts[x], (unsigned long long)s_cnt[x]);
+}
+template <int kKind>
+__global__ void k_dest_scatter(const uint64_t* __restrict__ keys, uint64_t m, uint32_t world, int bw,
+                               const uint32_t* __restrict__ gcuts, uint32_t p, const uint32_t* __restrict__ gowner,
+                               unsigned long long* __restrict__ cursor, uint64_t* __restrict__ out) {
+  extern __shared__ uint32_t sh[];
+  uint32_t* s_cuts = sh;
+  uint32_t* s_owner = s_cuts + p + 1;
+  if (kKind == 1) {
+    for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+    for (uint32_t x = threadIdx.x; x < p * (p + 1) / 2; x += blockDim.x) s_owner[x] = gowner[x];
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane;
+  for (uint64_t base = warp0; base < m; base += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = base + lane;
+    const bool valid = e < m;
+    const uint64_t k = valid ? keys[e] : 0;
+    const uint32_t w =
+        valid ? (kKind == 0 ? key_owner(k >> bw, world) : okey_owner(k, s_cuts, p, s_owner)) : 0xFFFFFFFFu;
+    // warp-aggregated reservation: one atomic per destination present in the warp
+    const uint32_t peers = __match_any_sync(0xffffffffu, w);
+    const uint32_t leader = __ffs(peers) - 1;
+    unsigned long long at = 0;
+    if (valid && lane == leader) at = atomicAdd(&cursor[w], (unsigned long long)__popc(peers));
+    at = __shfl_sync(peers, at, leader);
+    // kind 0 leaves in the wire form (lo << 32 | hi)
+    const uint64_t o = kKind == 0 ? ((k >> bw) << 32) | (k & ((1ull << bw) - 1)) : k;
+    if (valid) out[at + __popc(peers & ((1u << lane) - 1))] = o;
+  }
+}
+// Partial (this rank's) block sizes: fold the p x p part histogram into block order.
+__global__ void k_fold_blocks(const unsigned long long* __restrict__ hist, uint32_t p,
+                              unsigned long long* __restrict__ bnnz) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p; j += gridDim.x * blockDim.x)
+    for (uint32_t i = 0; i <= j; ++i) bnnz[j * (j + 1) / 2 + i] = hist[(uint64_t)i * p + j];
+}
+// Wire keys (lo << 32 | hi) -> narrow keys (lo << bw | hi) for sorting.
+__global__ void k_narrow(uint64_t* __restrict__ keys, uint64_t m, int bw) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    keys[e] = ((k >> 32) << bw) | (k & 0xFFFFFFFFull);
+  }
 }
 
 }  // namespace
@@ -649,6 +757,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   }
   if (m >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
   g->m = m;
+  g->m_total = m;
   // Degrees and stable degree rank.
   DevBuf<uint32_t> deg;
   deg.alloc(n, ctx);
@@ -983,6 +1092,14 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
     dim3 grid(std::max(1u, std::min((maxw + kThreads - 1) / kThreads, 64u)), std::min(nb, 16384u));
     k_col_local<<<grid, kThreads, 0, st>>>(plan->d_blocks.p, dco.p, nb, dcuts.p, out->p);
     BBTC_LAUNCHED(ctx);
+    const uint64_t items = plan->item_start.back();
+    plan->d_item_col.alloc(std::max<uint64_t>(items, 1), ctx);
+    if (items) {
+      k_item_cols<<<grid_for(ctx, items), kThreads, 0, st>>>(plan->d_tasks.p, plan->d_item_start.p,
+                                                             (uint32_t)plan->tasks.size(), items, plan->d_blocks.p,
+                                                             out->p, dco.p, plan->d_item_col.p);
+      BBTC_LAUNCHED(ctx);
+    }
   }
   // the streamed kernel finds block b's column offsets at co (BlockDesc.co)
   for (uint32_t b = 0; b < nb; ++b) plan->blocks[b].co = plan->co_off[b];
@@ -1067,6 +1184,289 @@ uint32_t plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget, uint32
   for (uint32_t p = hi / 2 + 1; p < hi; ++p)
     if (fits(p)) return p;
   return hi;
+}
+
+// =====================================================================================
+// §8(e) sharded build, one rank per GPU.  The caller (dist.py) moves the
+// buffers between ranks with NCCL; these are the per-rank device steps.
+
+// Sorted unique narrow keys (lo << bw | hi) of `keys[0, cnt)`, sentinels dropped; the
+// result is left in `keys` (swapped with a scratch buffer), the count returned.
+static uint64_t sort_unique(bbtc_ctx* ctx, DevBuf<uint64_t>& keys, uint64_t cnt, int bw) {
+  cudaStream_t st = ctx->stream;
+  if (!cnt) return 0;
+  DevBuf<uint64_t> alt;
+  alt.alloc(cnt, ctx);
+  cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
+  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, 2 * bw, st); },
+           radix_kernels(cnt, 2 * bw));
+  if (db.Current() != keys.p) std::swap(keys, alt);
+  DevBuf<uint64_t> nsel;
+  nsel.alloc(1, ctx);
+  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceSelect::Unique(t, b, keys.p, alt.p, nsel.p, cnt, st); });
+  uint64_t u = 0, last = 0;
+  BBTC_CUDA(cudaMemcpyAsync(&u, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  if (u) {
+    BBTC_CUDA(cudaMemcpyAsync(&last, alt.p + u - 1, 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  }
+  std::swap(keys, alt);
+  return u - (u && last == kSentinel ? 1 : 0);
+}
+
+// Groups keys[0, m) by destination rank into out (kind 0: canonical narrow keys by
+// key_owner, leaving in wire form; kind 1: oriented keys by block owner).
+template <int kKind>
+static void group_by_dest(bbtc_ctx* ctx, const uint64_t* keys, uint64_t m, uint32_t world, int bw,
+                          const uint32_t* dcuts, uint32_t p, const uint32_t* downer, uint64_t* out,
+                          uint64_t* send_counts) {
+  cudaStream_t st = ctx->stream;
+  DevBuf<unsigned long long> cnt;
+  cnt.alloc(world, ctx);
+  BBTC_CUDA(cudaMemsetAsync(cnt.p, 0, world * 8, st));
+  const uint32_t nb = p * (p + 1) / 2;
+  const size_t smem = 4 * ((size_t)world + (kKind == 1 ? p + 1 + nb : 0));
+  if (m) {
+    k_dest_count<kKind><<<grid_for(ctx, m), kThreads, smem, st>>>(keys, m, world, bw, dcuts, p, downer, cnt.p);
+    BBTC_LAUNCHED(ctx);
+  }
+  std::vector<unsigned long long> h(world), c0(world, 0);
+  BBTC_CUDA(cudaMemcpyAsync(h.data(), cnt.p, world * 8, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  for (uint32_t w = 1; w < world; ++w) c0[w] = c0[w - 1] + h[w - 1];
+  for (uint32_t w = 0; w < world; ++w) send_counts[w] = h[w];
+  BBTC_CUDA(cudaMemcpyAsync(cnt.p, c0.data(), world * 8, cudaMemcpyHostToDevice, st));
+  if (m) {
+    k_dest_scatter<kKind><<<grid_for(ctx, m), kThreads, smem, st>>>(keys, m, world, bw, dcuts, p, downer, cnt.p,
+                                                                      out);
+    BBTC_LAUNCHED(ctx);
+  }
+  BBTC_CUDA(cudaStreamSynchronize(st));   // (c0 is a host source of an async copy)
+}
+
+void shard_canon(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, int mem, uint32_t n_hint,
+                 uint32_t world, uint64_t* out, uint64_t* send_counts, uint32_t* max_id_plus1) {
+  cudaStream_t st = ctx->stream;
+  Trace tr(st, "shard_canon");
+  DevBuf<uint32_t> ds, dd;
+  if (mem == BBTC_MEM_HOST && E) {   // this rank's share of the raw edges crosses PCIe
+    ds.alloc(E, ctx);
+    dd.alloc(E, ctx);
+    BBTC_CUDA(cudaMemcpyAsync(ds.p, src, E * 4, cudaMemcpyHostToDevice, st));
+    BBTC_CUDA(cudaMemcpyAsync(dd.p, dst, E * 4, cudaMemcpyHostToDevice, st));
+    src = ds.p;
+    dst = dd.p;
+  }
+  tr.mark("h2d");
+  DevBuf<uint64_t> keys;
+  keys.alloc(std::max<uint64_t>(E, 1), ctx);
+  DevBuf<uint32_t> dmax;
+  dmax.alloc(1, ctx);
+  int bw = n_hint > 1 ? std::max(1, bitlen(n_hint - 1)) : 32;
+  uint32_t max_id = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    BBTC_CUDA(cudaMemsetAsync(dmax.p, 0, 4, st));
+    if (E) {
+      k_canon<<<grid_for(ctx, E), kThreads, 0, st>>>(src, dst, E, bw, keys.p, dmax.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    BBTC_CUDA(cudaMemcpyAsync(&max_id, dmax.p, 4, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    if (!E || bw == 32 || (max_id >> bw) == 0) break;
+    bw = 32;   // an id does not fit the hint's width
+  }
+  *max_id_plus1 = E ? max_id + 1 : 0;
+  tr.mark("canon");
+  const uint64_t u = sort_unique(ctx, keys, E, bw);
+  tr.mark("sort_unique");
+  group_by_dest<0>(ctx, keys.p, u, world, bw, nullptr, 1, nullptr, out, send_counts);
+  tr.mark("group");
+}
+
+void shard_graph(bbtc_ctx* ctx, const uint64_t* wire, uint64_t cnt, uint32_t n, uint32_t* d_deg, bbtc_graph* g) {
+  cudaStream_t st = ctx->stream;
+  Trace tr(st, "shard_graph");
+  const int bw = std::max(1, bitlen(n > 1 ? n - 1 : 1));
+  DevBuf<uint64_t> keys;
+  keys.alloc(std::max<uint64_t>(cnt, 1), ctx);
+  if (cnt) {
+    BBTC_CUDA(cudaMemcpyAsync(keys.p, wire, cnt * 8, cudaMemcpyDeviceToDevice, st));
+    k_narrow<<<grid_for(ctx, cnt), kThreads, 0, st>>>(keys.p, cnt, bw);
+    BBTC_LAUNCHED(ctx);
+  }
+  const uint64_t m = sort_unique(ctx, keys, cnt, bw);   // instances from several ranks meet here
+  tr.mark("sort_unique");
+  g->n = n;
+  g->m = m;
+  g->raw = cnt;
+  g->cbw = bw;
+  g->ckeys = std::move(keys);
+  BBTC_CUDA(cudaMemsetAsync(d_deg, 0, (size_t)n * 4, st));
+  if (m) {
+    k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(g->ckeys.p, m, bw, d_deg);
+    BBTC_LAUNCHED(ctx);
+  }
+  tr.mark("degree");
+}
+
+void shard_rank(bbtc_ctx* ctx, bbtc_graph* g, const uint32_t* d_deg, uint64_t m_total) {
+  cudaStream_t st = ctx->stream;
+  Trace tr(st, "shard_rank");
+  const uint32_t n = g->n;
+  const uint64_t m = g->m;
+  g->m_total = m_total;
+  g->deg_sorted.alloc(n, ctx);
+  g->rank.alloc(n, ctx);
+  g->okeys.alloc(m, ctx);
+  if (n) {
+    DevBuf<uint32_t> ids, order, dmax;
+    ids.alloc(n, ctx);
+    order.alloc(n, ctx);
+    dmax.alloc(2, ctx);
+    k_iota<<<grid_for(ctx, n), kThreads, 0, st>>>(ids.p, n);
+    BBTC_LAUNCHED(ctx);
+    const int bdeg = std::max(1, bitlen(std::min<uint64_t>(m_total, n - 1)));
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, d_deg, g->deg_sorted.p, ids.p, order.p, (uint64_t)n, 0, bdeg, st);
+    }, radix_kernels(n, bdeg));
+    k_rank<<<grid_for(ctx, n), kThreads, 0, st>>>(order.p, n, g->rank.p);
+    BBTC_LAUNCHED(ctx);
+    if (m) {
+      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(g->ckeys.p, m, g->cbw, g->rank.p, g->okeys.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    k_graph_stats<<<1, 32, 0, st>>>(g->deg_sorted.p, n, dmax.p);
+    BBTC_LAUNCHED(ctx);
+    uint32_t h[2];
+    BBTC_CUDA(cudaMemcpyAsync(h, dmax.p, 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    g->n_nonisolated = n - h[0];
+    g->d_max = h[1];
+  }
+  g->ckeys.reset();
+  tr.mark("rank_orient");
+}
+
+uint32_t shard_blocks_hist(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts,
+                           uint64_t* d_bnnz, uint32_t* cuts_out) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = g->n;
+  std::vector<uint32_t> cuts;
+  uint32_t pe = p;
+  if (user_cuts) {
+    if (user_cuts[0] != 0 || user_cuts[p] != n) raise(BBTC_EINVAL, "cuts must satisfy cuts[0] = 0 and cuts[p] = n");
+    for (uint32_t i = 0; i < p; ++i)
+      if (user_cuts[i] > user_cuts[i + 1]) raise(BBTC_EINVAL, "cuts must be non-decreasing");
+    cuts.assign(user_cuts, user_cuts + p + 1);
+  } else {
+    pe = n == 0 ? 1 : std::min(p, n);
+    cuts.assign(pe + 1, 0);
+    cuts[pe] = n;
+    if (n > 0 && pe > 1) {   // the default rule over the GLOBAL degrees (P[n] = 2 m_total)
+      DevBuf<uint64_t> incl;
+      incl.alloc(n, ctx);
+      cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(g->deg_sorted.p, ToU64{});
+      cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, it, incl.p, (uint64_t)n, st); });
+      DevBuf<uint32_t> dc;
+      dc.alloc(pe + 1, ctx);
+      k_cuts<<<1, 256, 0, st>>>(incl.p, n, 2 * g->m_total, pe, dc.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaMemcpyAsync(cuts.data(), dc.p, (pe + 1) * 4, cudaMemcpyDeviceToHost, st));
+      BBTC_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  std::copy(cuts.begin(), cuts.end(), cuts_out);
+  DevBuf<uint32_t> dc;
+  dc.alloc(pe + 1, ctx);
+  BBTC_CUDA(cudaMemcpyAsync(dc.p, cuts.data(), (pe + 1) * 4, cudaMemcpyHostToDevice, st));
+  DevBuf<unsigned long long> hist;
+  hist.alloc((uint64_t)pe * pe, ctx);
+  BBTC_CUDA(cudaMemsetAsync(hist.p, 0, (uint64_t)pe * pe * 8, st));
+  if (g->m) {
+    const bool sm = (uint64_t)pe * pe <= 8192;
+    const size_t smem = 4 * ((size_t)pe + 1 + (sm ? (size_t)pe * pe : 0));
+    k_part_hist<<<grid_for(ctx, g->m), kThreads, smem, st>>>(g->okeys.p, g->m, dc.p, pe, sm, hist.p);
+    BBTC_LAUNCHED(ctx);
+  }
+  k_fold_blocks<<<1, 256, 0, st>>>(hist.p, pe, (unsigned long long*)d_bnnz);
+  BBTC_LAUNCHED(ctx);
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  return pe;
+}
+
+void shard_by_block(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts, const uint32_t* owner,
+                    uint32_t world, uint64_t* out, uint64_t* send_counts) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t nb = p * (p + 1) / 2;
+  DevBuf<uint32_t> dc, dow;
+  dc.alloc(p + 1, ctx);
+  dow.alloc(nb, ctx);
+  BBTC_CUDA(cudaMemcpyAsync(dc.p, cuts, (p + 1) * 4, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemcpyAsync(dow.p, owner, nb * 4, cudaMemcpyHostToDevice, st));
+  group_by_dest<1>(ctx, g->okeys.p, g->m, world, 32, dc.p, p, dow.p, out, send_counts);
+}
+
+// The rank's plan in the global block layout: the blocks it owns built from the
+// oriented edges it received (every edge of those blocks), the other blocks allocated
+// at their global offsets and empty until the caller moves them in.
+void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* okeys, uint64_t cnt, uint32_t p,
+                      const uint32_t* cuts, const uint64_t* bnnz, const uint32_t* task_rank, uint32_t rank,
+                      uint32_t world, uint32_t flags, bbtc_plan* plan) {
+  cudaStream_t st = ctx->stream;
+  Trace tr(st, "plan_build_shard");
+  bbtc_graph tg;
+  tg.ctx = ctx;
+  tg.n = like->n;
+  tg.m = cnt;
+  tg.m_total = like->m_total;
+  tg.n_nonisolated = like->n_nonisolated;
+  tg.d_max = like->d_max;
+  tg.okeys.alloc(std::max<uint64_t>(cnt, 1), ctx);
+  if (cnt) BBTC_CUDA(cudaMemcpyAsync(tg.okeys.p, okeys, cnt * 8, cudaMemcpyDeviceToDevice, st));
+  const uint64_t n_tasks_all = n_tasks(p);
+  plan->task_rank.assign(task_rank, task_rank + n_tasks_all);
+  plan->shard_rank = rank;
+  plan->shard_world = world;
+  plan_build(ctx, &tg, p, cuts, flags & ~BBTC_PLAN_STATS, plan);
+  tr.mark("local_build");
+  // Re-lay the arenas out at the global block offsets.
+  const uint32_t nb = p * (p + 1) / 2;
+  uint64_t mg = 0, m_max = 0, bytes = 0;
+  std::vector<uint64_t> e0g(nb);
+  for (uint32_t b = 0; b < nb; ++b) {
+    e0g[b] = mg;
+    mg += bnnz[b];
+    m_max = std::max<uint64_t>(m_max, bnnz[b]);
+    const BlockDesc& B = plan->blocks[b];
+    if (B.nnz && B.nnz != bnnz[b])
+      raise(BBTC_EINVAL, "shard plan: a block received " + std::to_string(B.nnz) + " of its " +
+                             std::to_string(bnnz[b]) + " edges (every edge of an owned block must be sent to its owner)");
+  }
+  if (mg >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
+  for (auto& A : plan->edge_arenas()) {
+    DevBuf<uint32_t> g;
+    g.alloc(std::max<uint64_t>(mg, 1), ctx);
+    for (uint32_t b = 0; b < nb; ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      if (B.nnz) BBTC_CUDA(cudaMemcpyAsync(g.p + e0g[b], A.dev->p + B.e0, B.nnz * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    *A.dev = std::move(g);
+  }
+  for (uint32_t b = 0; b < nb; ++b) {
+    BlockDesc& B = plan->blocks[b];
+    B.e0 = e0g[b];
+    B.nnz = bnnz[b];
+    bytes += 4 * plan->edge_arenas().size() * B.nnz + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1);
+  }
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
+  plan->m = mg;
+  plan->info.m = mg;
+  plan->info.m_max = m_max;
+  plan->info.lambda = mg ? (double)m_max / (2.0 * (double)mg / ((double)p * (p + 1))) : 1.0;
+  plan->info.block_bytes = bytes;
+  plan_tasks(plan, 1);   // this rank's tasks only, in the global block layout
+  tr.mark("relayout");
 }
 
 }  // namespace bbtc

@@ -69,7 +69,7 @@ def run(spec, p, modes, row_major=False):
                 out[mode + "_h2d"] = int(tm["h2d_bytes"])
             elif mode.startswith("ooc"):
                 frac = int(mode[3:]) / 100
-                budget = max(int(whole * frac), int(max_task * 1.05))
+                budget = max(int(whole * frac), int(max_task * 2))
                 plan.set_budget(budget)
                 t, pt, tm = plan.count(timing=True)
                 plan.set_budget(0)
