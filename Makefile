@@ -11,7 +11,7 @@ NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC,-fvisibility=hidde
             --expt-relaxed-constexpr -Xptxas -v
 CXXFLAGS := -std=c++17 -O3 -fPIC -Iinclude
 
-LIB_SRCS := $(CSRC)/capi.cpp $(CSRC)/io.cpp $(CSRC)/prep.cu $(CSRC)/count.cu
+LIB_SRCS := $(CSRC)/capi.cpp $(CSRC)/io.cpp $(CSRC)/cpu.cpp $(CSRC)/prep.cu $(CSRC)/count.cu
 LIB_HDRS := include/bbtc.h $(CSRC)/internal.h
 
 all: $(PKG)/libbbtc.so oracle/liboracle.so inputs/libbbtcgen.so
@@ -30,7 +30,11 @@ build/io.o: $(CSRC)/io.cpp $(LIB_HDRS)
 	@mkdir -p build
 	$(NVCC) -std=c++17 -O3 -Xcompiler -fPIC,-fvisibility=hidden -Iinclude -x cu $(ARCH) -c $< -o $@
 
-$(PKG)/libbbtc.so: build/capi.o build/io.o build/prep.o build/count.o
+build/cpu.o: $(CSRC)/cpu.cpp $(LIB_HDRS)
+	@mkdir -p build
+	$(NVCC) -std=c++17 -O3 -Xcompiler -fPIC,-fvisibility=hidden -Iinclude -x cu $(ARCH) -c $< -o $@
+
+$(PKG)/libbbtc.so: build/capi.o build/io.o build/cpu.o build/prep.o build/count.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -lpthread
 
 oracle/liboracle.so: oracle/oracle.cpp

@@ -279,6 +279,51 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
 BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world,
                                 uint32_t flags, uint64_t* total, uint64_t* per_task, bbtc_timing* t);
 
+/* §8(f)#4 study support.  bbtc_plan_block_nnz: nnz of every block, HOST uint64[p(p+1)/2]
+ * (block order b = j(j+1)/2 + i).  bbtc_task_times: device time of every task alone
+ * (HOST double[n_tasks], canonical order, milliseconds; CUDA events around one launch of
+ * the task's own work items — list or bit-row kernel), for ranking workload estimators
+ * against measured task times.  Needs resident blocks.  Slow (one launch
+ * per task): a study tool, not a counting path. */
+BBTC_API bbtc_status bbtc_plan_block_nnz(const bbtc_plan* plan, uint64_t* nnz);
+BBTC_API bbtc_status bbtc_task_times(bbtc_ctx* ctx, const bbtc_plan* plan, double* ms);
+/* A PBD-like refinement of a cut vector (P:459-460 cite PBD without describing it; SPEC's
+ * reading: move interior cuts while the largest block m_max strictly decreases): pattern
+ * search over each interior cut with steps halving from |V_i|/2 to 1, every candidate
+ * evaluated exactly by one pass over the oriented edges (block histogram); at most
+ * max_evals evaluations.  cuts_in: HOST uint32[p+1] (NULL = the default rule);
+ * cuts_out: HOST uint32[p+1]; *m_max_out: the largest block nnz of cuts_out.  The
+ * result is a valid symmetric partition whatever it converges to. */
+BBTC_API bbtc_status bbtc_cuts_refine(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts_in,
+                                      uint32_t max_evals, uint32_t* cuts_out, uint64_t* m_max_out);
+
+/* §8(f)#3 hybrid CPU+GPU count (Alg. 8, §7.7).  The sparse tasks are
+ * queued by the paper's ExecTime estimate nnz(G_ij)·max(δ(G_ik), δ(G_jk)), heaviest
+ * first.  The GPU (the calling thread drives it) claims the front of the
+ * queue up to the cut-off, then further chunks while tasks remain (one list-kernel
+ * launch per claim, over a task table of its own); cpu_threads host threads claim single
+ * tasks from the back and never pass the cut-off, each counting its task
+ * with Alg. 6's dense map over V_k (a bitmap) on the plan's pinned host
+ * arenas.  Dense (bit-row) tasks stay on the GPU.  Requires a plan with host arenas
+ * (bbtc_plan_to_host) that is also device-resident (bbtc_stage): the split is measured
+ * "excl. H2D".  Results as bbtc_count (rank 0 of 1). */
+typedef struct {
+  uint32_t cpu_threads;   /* host threads (0 = hardware concurrency) */
+  uint32_t gpu_chunk;     /* tasks per GPU claim past the cut-off (0 = 1/8 of what is left) */
+  double cutoff;          /* GPU-reserved front of the queue, fraction of the sparse tasks
+                             (paper default 0.5; 1 = GPU only, 0 = no reservation) */
+} bbtc_hybrid_opts;
+typedef struct {
+  uint64_t cpu_tasks, gpu_tasks;   /* sparse tasks counted by each side */
+  uint64_t gpu_launches;           /* list-kernel launches (claims) */
+  uint64_t cpu_triangles;          /* triangles found by the CPU threads */
+  double t_cpu_ms;                 /* wall time until the last CPU thread finished */
+  double t_gpu_ms;                 /* wall time until the GPU's last claim finished */
+} bbtc_hybrid_stats;
+BBTC_API bbtc_status bbtc_count_hybrid(bbtc_ctx* ctx, const bbtc_plan* plan, const bbtc_hybrid_opts* opts,
+                                       uint64_t* total, uint64_t* per_task, bbtc_timing* t,
+                                       bbtc_hybrid_stats* stats);
+
 /* a6: makes every block of a host-resident plan resident on the context's
  * device (so a following count runs "excl. H2D").  No-op for device plans. */
 BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan);

@@ -169,6 +169,18 @@ class Graph:
         self.close()
 
 
+def refine_cuts(ctx: "Context", graph: "Graph", p: int, cuts=None, max_evals: int = 200):
+    """bbtc_cuts_refine (§8(f)#4): PBD-like cuts minimising m_max; returns (cuts, m_max)."""
+    out = np.empty(p + 1, np.uint32)
+    mm = ctypes.c_uint64()
+    cin = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.uint32)
+    L.check(L.bbtc_cuts_refine(ctx.handle, graph._h, p, None if cin is None else cin.ctypes.data_as(L._u32p),
+                               max_evals, out.ctypes.data_as(L._u32p), ctypes.byref(mm)))
+    n = graph.n
+    pe = p if cin is not None else (min(p, n) if n else 1)   # the default rule clamps p to n
+    return out[:pe + 1].copy(), int(mm.value)
+
+
 def auto_p(ctx: "Context", graph: "Graph", budget_bytes: int, depth: int = 2, row_major: bool = False) -> int:
     """bbtc_plan_auto_p: the smallest p whose largest task footprint x depth fits the budget."""
     p = ctypes.c_uint32()
@@ -252,6 +264,34 @@ class Plan:
         if timing:
             return int(tot.value), pt, {f: getattr(tm, f) for f, _ in tm._fields_}
         return int(tot.value), pt
+
+    def block_nnz(self) -> np.ndarray:
+        """nnz of every block, block order b = j(j+1)/2 + i (bbtc_plan_block_nnz)."""
+        p = self.p
+        out = np.empty(p * (p + 1) // 2, np.uint64)
+        L.check(L.bbtc_plan_block_nnz(self._h, out.ctypes.data_as(L._u64p)))
+        return out
+
+    def task_times(self) -> np.ndarray:
+        """Device ms of every task alone, canonical order (bbtc_task_times; a study tool)."""
+        out = np.empty(self.n_tasks, np.float64)
+        L.check(L.bbtc_task_times(self.ctx.handle, self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def count_hybrid(self, cpu_threads: int = 0, cutoff: float = 0.5, gpu_chunk: int = 0):
+        """bbtc_count_hybrid (§8(f)#3): GPU from the heavy end of the ExecTime queue, CPU threads
+        from the light end up to the cut-off.  Needs to_host() + stage().  Returns
+        (total, per_task, stats dict)."""
+        tot = ctypes.c_uint64()
+        pt = np.zeros(self.n_tasks, np.uint64)
+        o = L.bbtc_hybrid_opts(cpu_threads, gpu_chunk, cutoff)
+        tm = L.bbtc_timing()
+        hs = L.bbtc_hybrid_stats()
+        L.check(L.bbtc_count_hybrid(self.ctx.handle, self._h, ctypes.byref(o), ctypes.byref(tot),
+                                    pt.ctypes.data_as(L._u64p), ctypes.byref(tm), ctypes.byref(hs)))
+        st = {f: getattr(hs, f) for f, _ in hs._fields_}
+        st["t_total_ms"] = tm.t_total_ms
+        return int(tot.value), pt, st
 
     def count_async(self, d_counts, rank: int = 0, world: int = 1):
         """Enqueue the count into a CUDA uint64/int64 tensor of n_tasks+1 entries (last = total)."""

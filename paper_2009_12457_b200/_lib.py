@@ -73,6 +73,15 @@ class bbtc_block_ptrs(ctypes.Structure):
                 ("rowptr", _vp), ("rowptr_len", c_u64)]
 
 
+class bbtc_hybrid_opts(ctypes.Structure):
+    _fields_ = [("cpu_threads", c_u32), ("gpu_chunk", c_u32), ("cutoff", ctypes.c_double)]
+
+
+class bbtc_hybrid_stats(ctypes.Structure):
+    _fields_ = [("cpu_tasks", c_u64), ("gpu_tasks", c_u64), ("gpu_launches", c_u64), ("cpu_triangles", c_u64),
+                ("t_cpu_ms", ctypes.c_double), ("t_gpu_ms", ctypes.c_double)]
+
+
 def _sig(name, res, *args):
     f = getattr(lib, name)
     f.restype = res
@@ -107,6 +116,11 @@ bbtc_task_index = _sig("bbtc_task_index", _st, c_u32, c_u32, c_u32, c_u32, _u64p
 bbtc_task_ijk = _sig("bbtc_task_ijk", _st, c_u32, c_u64, _u32p, _u32p, _u32p)
 bbtc_count_async = _sig("bbtc_count_async", _st, _vp, _vp, c_u32, c_u32, _vp)
 bbtc_count = _sig("bbtc_count", _st, _vp, _vp, c_u32, c_u32, c_u32, _u64p, _u64p, ctypes.POINTER(bbtc_timing))
+bbtc_count_hybrid = _sig("bbtc_count_hybrid", _st, _vp, _vp, ctypes.POINTER(bbtc_hybrid_opts), _u64p, _u64p,
+                         ctypes.POINTER(bbtc_timing), ctypes.POINTER(bbtc_hybrid_stats))
+bbtc_plan_block_nnz = _sig("bbtc_plan_block_nnz", _st, _vp, _u64p)
+bbtc_task_times = _sig("bbtc_task_times", _st, _vp, _vp, ctypes.POINTER(ctypes.c_double))
+bbtc_cuts_refine = _sig("bbtc_cuts_refine", _st, _vp, _vp, c_u32, _u32p, c_u32, _u32p, _u64p)
 bbtc_stage = _sig("bbtc_stage", _st, _vp, _vp)
 bbtc_unstage = _sig("bbtc_unstage", _st, _vp, _vp)
 bbtc_shard_canon = _sig("bbtc_shard_canon", _st, _vp, _vp, _vp, c_u64, ctypes.c_int, c_u32, c_u32, _vp, _u64p,

@@ -9,6 +9,10 @@
 #include <stdexcept>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
+#include <mutex>
+#include <thread>
+#include <atomic>
 
 #include "internal.h"
 
@@ -577,7 +581,7 @@ static void ensure_device_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
 static void finish_full_arenas(bbtc_ctx* ctx, bbtc_plan* plan) {
   if (!plan->streams_colptr()) return;
   colptr_expand_all(ctx, plan);
-  plan->d_colptr.reset();
+  if (!getenv("BBTC_FORCE_CP")) plan->d_colptr.reset();   // (A/B knob: keep it for resident kCP counts)
 }
 
 }  // namespace bbtc
@@ -1039,7 +1043,19 @@ static void stream_order(bbtc_ctx* ctx, bbtc_plan* plan) {
 static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                            cudaEvent_t mid = nullptr) {
   dense_build(ctx, plan);
-  count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0);
+  if (getenv("BBTC_FORCE_CP") && plan->d_colptr.p && plan->d_item_col.p) {
+    // A/B: the streamed walk (column offsets, kCP) over resident blocks
+    DevArenas ar;
+    ar.cols = plan->cols.p;
+    ar.it_u = plan->ccu.p;
+    ar.rowptr = plan->rowptr.p;
+    ar.blocks = plan->d_blocks.p;
+    ar.colptr = plan->d_colptr.p;
+    ar.item_col = plan->d_item_col.p;
+    count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0, &ar);
+  } else {
+    count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0);
+  }
   if (mid) BBTC_CUDA(cudaEventRecord(mid, ctx->stream));
   count_launch_dense(ctx, plan, rank, world, d_counts, plan->dense_item_lo, plan->item_start.back());
 }
@@ -1058,6 +1074,184 @@ BBTC_API bbtc_status bbtc_count_async(bbtc_ctx* ctx, const bbtc_plan* plan, uint
       world = 1;
     }
     count_resident(ctx, const_cast<bbtc_plan*>(plan), rank, world, d_counts);
+  });
+}
+
+// ---- §8(f)#4 study support ------------------------------------------------------------
+BBTC_API bbtc_status bbtc_plan_block_nnz(const bbtc_plan* plan, uint64_t* nnz) {
+  return guard([&] {
+    if (!plan || !nnz) raise(BBTC_EINVAL, "NULL argument");
+    for (size_t b = 0; b < plan->blocks.size(); ++b) nnz[b] = plan->blocks[b].nnz;
+  });
+}
+
+BBTC_API bbtc_status bbtc_task_times(bbtc_ctx* ctx, const bbtc_plan* cplan, double* ms) {
+  return guard([&] {
+    if (!ctx || !cplan || !ms) raise(BBTC_EINVAL, "NULL argument");
+    bbtc_plan* plan = const_cast<bbtc_plan*>(cplan);
+    if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t nt = plan->info.n_tasks;
+    std::fill(ms, ms + nt, 0.0);
+    DevBuf<uint64_t> d_counts;
+    d_counts.alloc(nt + 1, ctx);
+    count_zero(ctx, plan, d_counts.p);
+    dense_build(ctx, plan);
+    cudaEvent_t a, b;
+    BBTC_CUDA(cudaEventCreate(&a));
+    BBTC_CUDA(cudaEventCreate(&b));
+    for (size_t t = 0; t < plan->tasks.size(); ++t) {
+      const uint64_t lo = plan->item_start[t], hi = plan->item_start[t + 1];
+      BBTC_CUDA(cudaEventRecord(a, ctx->stream));
+      if (hi > lo) {
+        if (t < plan->dense_task_lo) count_launch(ctx, plan, 0, 1, d_counts.p, lo, hi, nullptr, 0);
+        else count_launch_dense(ctx, plan, 0, 1, d_counts.p, lo, hi);
+      }
+      BBTC_CUDA(cudaEventRecord(b, ctx->stream));
+      BBTC_CUDA(cudaEventSynchronize(b));
+      float f = 0;
+      BBTC_CUDA(cudaEventElapsedTime(&f, a, b));
+      ms[plan->tasks[t].idx] = f;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+BBTC_API bbtc_status bbtc_cuts_refine(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts_in,
+                                      uint32_t max_evals, uint32_t* cuts_out, uint64_t* m_max_out) {
+  return guard([&] {
+    if (!ctx || !g || !cuts_out || !m_max_out) raise(BBTC_EINVAL, "NULL argument");
+    if (p == 0 || p > 4096) raise(BBTC_EINVAL, "need 1 <= p <= 4096");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    cuts_refine(ctx, g, p, cuts_in, max_evals, cuts_out, m_max_out);
+  });
+}
+
+// ---- §8(f)#3 hybrid CPU+GPU (cpu.cpp holds the CPU side) -----------------------------
+BBTC_API bbtc_status bbtc_count_hybrid(bbtc_ctx* ctx, const bbtc_plan* cplan, const bbtc_hybrid_opts* o,
+                                       uint64_t* total, uint64_t* per_task, bbtc_timing* tm,
+                                       bbtc_hybrid_stats* hs) {
+  return guard([&] {
+    if (!ctx || !cplan || !total) raise(BBTC_EINVAL, "NULL argument");
+    bbtc_plan* plan = const_cast<bbtc_plan*>(cplan);
+    if (!plan->host_blocks || !plan->resident)
+      raise(BBTC_ESTATE, "hybrid counts need host arenas (bbtc_plan_to_host) and resident blocks (bbtc_stage)");
+    if (plan->shard_world) raise(BBTC_EINVAL, "hybrid counts take whole plans, not shards");
+    bbtc_hybrid_opts opt{0, 0, 0.5};
+    if (o) opt = *o;
+    if (!(opt.cutoff >= 0.0 && opt.cutoff <= 1.0)) raise(BBTC_EINVAL, "cutoff must be in [0, 1]");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const uint64_t l0 = ctx->launches;
+    const uint64_t nt = plan->info.n_tasks;
+    DevBuf<uint64_t> d_counts;
+    d_counts.alloc(nt + 1, ctx);
+    count_zero(ctx, plan, d_counts.p);
+    const std::vector<uint32_t> q = exec_time_queue(plan);   // execution-order task positions
+    const uint64_t n = q.size();
+    const uint64_t cut = (uint64_t)std::ceil(opt.cutoff * (double)n);
+    std::mutex mu;
+    uint64_t front = 0, back = n;   // [front, back) unclaimed
+    // CPU threads: single tasks from the back, never below the cut-off
+    unsigned nth = opt.cpu_threads ? opt.cpu_threads : std::max(1u, std::thread::hardware_concurrency());
+    if (cut >= n) nth = 0;
+    std::vector<std::vector<uint64_t>> cpu_pt(nth, std::vector<uint64_t>(nt, 0));
+    std::vector<uint64_t> cpu_done(nth, 0);
+    std::atomic<int64_t> cpu_end_us{0};
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nth; ++w)
+      pool.emplace_back([&, w] {
+        std::vector<uint64_t> bits;
+        for (;;) {
+          uint64_t t;
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            if (back <= std::max(front, cut)) break;
+            t = --back;
+          }
+          const TaskDesc& T = plan->tasks[q[t]];
+          cpu_pt[w][T.idx] += cpu_count_task(plan, T, bits);
+          cpu_done[w]++;
+        }
+        const int64_t us = std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t0).count();
+        int64_t prev = cpu_end_us.load();
+        while (prev < us && !cpu_end_us.compare_exchange_weak(prev, us)) {}
+      });
+    // GPU: the front up to the cut-off, then chunks while tasks remain; one launch per
+    // claim over its own task table, the next claim after the previous launch ends.
+    std::vector<DevBuf<TaskDesc>> tabs;
+    std::vector<DevBuf<uint64_t>> starts;
+    std::vector<std::vector<TaskDesc>> h_tabs;
+    std::vector<std::vector<uint64_t>> h_starts;
+    uint64_t gpu_tasks = 0, claims = 0;
+    for (bool first = true;; first = false) {
+      uint64_t a, b;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (front >= back) break;
+        a = front;
+        const uint64_t left = back - front;
+        const uint64_t take = first ? std::max<uint64_t>(cut, std::min<uint64_t>(left, 1))
+                                    : (opt.gpu_chunk ? opt.gpu_chunk : std::max<uint64_t>(1, left / 8));
+        b = std::min(back, a + std::max<uint64_t>(take, 1));
+        front = b;
+      }
+      h_tabs.emplace_back();
+      h_starts.emplace_back(1, 0);
+      for (uint64_t x = a; x < b; ++x) {
+        const uint32_t t = q[x];
+        h_tabs.back().push_back(plan->tasks[t]);
+        h_starts.back().push_back(h_starts.back().back() + plan->item_start[t + 1] - plan->item_start[t]);
+      }
+      tabs.emplace_back();
+      starts.emplace_back();
+      tabs.back().alloc(h_tabs.back().size(), ctx);
+      starts.back().alloc(h_starts.back().size(), ctx);
+      BBTC_CUDA(cudaMemcpyAsync(tabs.back().p, h_tabs.back().data(), h_tabs.back().size() * sizeof(TaskDesc),
+                                cudaMemcpyHostToDevice, ctx->stream));
+      BBTC_CUDA(cudaMemcpyAsync(starts.back().p, h_starts.back().data(), h_starts.back().size() * 8,
+                                cudaMemcpyHostToDevice, ctx->stream));
+      count_launch(ctx, plan, 0, 1, d_counts.p, 0, h_starts.back().back(), nullptr, 0, nullptr, tabs.back().p,
+                   starts.back().p, (uint32_t)h_tabs.back().size());
+      gpu_tasks += b - a;
+      ++claims;
+      BBTC_CUDA(cudaStreamSynchronize(ctx->stream));   // a claim ends before the next one
+    }
+    const double t_gpu = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    // dense tasks stay on the GPU
+    dense_build(ctx, plan);
+    count_launch_dense(ctx, plan, 0, 1, d_counts.p, plan->dense_item_lo, plan->item_start.back());
+    std::vector<uint64_t> h(nt + 1);
+    BBTC_CUDA(cudaMemcpyAsync(h.data(), d_counts.p, (nt + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& th : pool) th.join();
+    uint64_t cpu_tri = 0, cpu_tasks = 0;
+    for (unsigned w = 0; w < nth; ++w) {
+      cpu_tasks += cpu_done[w];
+      for (uint64_t t = 0; t < nt; ++t) {
+        h[t] += cpu_pt[w][t];
+        cpu_tri += cpu_pt[w][t];
+      }
+    }
+    h[nt] += cpu_tri;
+    *total = h[nt];
+    if (per_task) std::copy(h.begin(), h.begin() + nt, per_task);
+    const double t_all = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    if (tm) {
+      std::memset(tm, 0, sizeof(*tm));
+      tm->t_total_ms = t_all;
+      tm->launches = ctx->launches - l0;
+    }
+    if (hs) {
+      hs->cpu_tasks = cpu_tasks;
+      hs->gpu_tasks = gpu_tasks;
+      hs->gpu_launches = claims;
+      hs->cpu_triangles = cpu_tri;
+      hs->t_cpu_ms = cpu_end_us.load() / 1e3;
+      hs->t_gpu_ms = t_gpu;
+    }
   });
 }
 

@@ -682,7 +682,7 @@ void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts) {
 // execution order (this rank's residues only), accumulating into d_counts.
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                   uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch, const DevArenas* ar,
-                  const TaskDesc* tasks, const uint64_t* item_start) {
+                  const TaskDesc* tasks, const uint64_t* item_start, uint32_t n_exec) {
   cudaStream_t st = ctx->stream;
   const uint64_t nt = plan->info.n_tasks;
   if (item_hi <= item_lo + rank) return;
@@ -745,7 +745,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
-      (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
+      n_exec ? n_exec : (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
       (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col);
   BBTC_LAUNCHED(ctx);
 }

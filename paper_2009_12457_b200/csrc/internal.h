@@ -251,7 +251,7 @@ void count_zero(bbtc_ctx* ctx, const bbtc_plan* plan, uint64_t* d_counts);
 void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                   uint64_t item_lo, uint64_t item_hi, const uint32_t* ready, uint32_t epoch,
                   const DevArenas* arenas = nullptr, const TaskDesc* tasks = nullptr,
-                  const uint64_t* item_start = nullptr);
+                  const uint64_t* item_start = nullptr, uint32_t n_exec = 0);
 void plan_stats(bbtc_ctx* ctx, bbtc_plan* plan);
 uint32_t plan_auto_p(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t budget, uint32_t depth, uint32_t flags);
 // Dense tasks: build the bit rows (once per resident plan) and count items
@@ -264,6 +264,12 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, bbtc::DevBuf<uint32_t>* ou
 void colptr_expand_all(bbtc_ctx* ctx, bbtc_plan* plan);
 void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                         uint64_t item_lo, uint64_t item_hi);
+// §8(f)#4 PBD-like cut refinement (prep.cu)
+void cuts_refine(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts_in, uint32_t max_evals,
+                 uint32_t* cuts_out, uint64_t* m_max_out);
+// §8(f)#3 hybrid (cpu.cpp)
+uint64_t cpu_count_task(const bbtc_plan* plan, const TaskDesc& T, std::vector<uint64_t>& bits);
+std::vector<uint32_t> exec_time_queue(const bbtc_plan* plan);
 // §8(e) sharded build (prep.cu)
 void shard_canon(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, int mem, uint32_t n_hint,
                  uint32_t world, uint64_t* out, uint64_t* send_counts, uint32_t* max_id_plus1);

@@ -1469,4 +1469,73 @@ void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* oke
   tr.mark("relayout");
 }
 
+// §8(f)#4: PBD-like refinement of a cut vector, minimising the largest block m_max
+// (the λ of P:573-586).  Pattern search: for each interior cut, try moving it by
+// ±step (clamped between its neighbours) and keep a move when m_max strictly
+// decreases; halve the step when a full sweep keeps nothing.  Every candidate is
+// evaluated exactly (one pass over the oriented edges: the p x p block histogram).
+void cuts_refine(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* cuts_in, uint32_t max_evals,
+                 uint32_t* cuts_out, uint64_t* m_max_out) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t n = g->n;
+  std::vector<uint32_t> cuts;
+  uint32_t pe = p;
+  if (cuts_in) {
+    if (cuts_in[0] != 0 || cuts_in[p] != n) raise(BBTC_EINVAL, "cuts must satisfy cuts[0] = 0 and cuts[p] = n");
+    for (uint32_t i = 0; i < p; ++i)
+      if (cuts_in[i] > cuts_in[i + 1]) raise(BBTC_EINVAL, "cuts must be non-decreasing");
+    cuts.assign(cuts_in, cuts_in + p + 1);
+  } else {
+    DevBuf<uint64_t> dn;
+    dn.alloc(std::max<uint32_t>(p * (p + 1) / 2, 1), ctx);
+    cuts.resize(p + 1);
+    pe = shard_blocks_hist(ctx, g, p, nullptr, dn.p, cuts.data());   // the default rule
+    cuts.resize(pe + 1);
+  }
+  DevBuf<uint32_t> dc;
+  dc.alloc(pe + 1, ctx);
+  DevBuf<unsigned long long> hist;
+  hist.alloc((uint64_t)pe * pe, ctx);
+  std::vector<unsigned long long> h((uint64_t)pe * pe);
+  uint32_t evals = 0;
+  auto m_max = [&](const std::vector<uint32_t>& c) {
+    ++evals;
+    BBTC_CUDA(cudaMemcpyAsync(dc.p, c.data(), (pe + 1) * 4, cudaMemcpyHostToDevice, st));
+    BBTC_CUDA(cudaMemsetAsync(hist.p, 0, (uint64_t)pe * pe * 8, st));
+    if (g->m) {
+      const bool sm = (uint64_t)pe * pe <= 8192;
+      const size_t smem = 4 * ((size_t)pe + 1 + (sm ? (size_t)pe * pe : 0));
+      k_part_hist<<<grid_for(ctx, g->m), kThreads, smem, st>>>(g->okeys.p, g->m, dc.p, pe, sm, hist.p);
+      BBTC_LAUNCHED(ctx);
+    }
+    BBTC_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+    return (uint64_t)*std::max_element(h.begin(), h.end());
+  };
+  uint64_t best = m_max(cuts);
+  uint32_t step = 1;
+  for (uint32_t i = 0; i < pe; ++i) step = std::max(step, (cuts[i + 1] - cuts[i]) / 2);
+  while (step >= 1 && evals < max_evals && pe > 1) {
+    bool moved = false;
+    for (uint32_t i = 1; i < pe && evals < max_evals; ++i)
+      for (int dir : {-1, 1}) {
+        if (evals >= max_evals) break;
+        std::vector<uint32_t> c = cuts;
+        const int64_t v = (int64_t)c[i] + dir * (int64_t)step;
+        c[i] = (uint32_t)std::min<int64_t>(std::max<int64_t>(v, c[i - 1]), c[i + 1]);
+        if (c[i] == cuts[i]) continue;
+        const uint64_t mm = m_max(c);
+        if (mm < best) {
+          best = mm;
+          cuts = c;
+          moved = true;
+        }
+      }
+    if (!moved) step /= 2;
+  }
+  std::fill(cuts_out, cuts_out + p + 1, 0u);
+  std::copy(cuts.begin(), cuts.end(), cuts_out);
+  *m_max_out = best;
+}
+
 }  // namespace bbtc

@@ -469,3 +469,57 @@ def test_packed_transpose_keys(gpu):
     for tot, pt, cuts in json.loads(res.stdout.strip().splitlines()[-1]):
         otot, opt, _, _ = og.count(cuts=np.asarray(cuts, np.uint32))
         assert tot == otot and pt == [int(x) for x in opt]
+
+
+@pytest.mark.parametrize("cutoff,threads", [(0.0, 4), (0.5, 0), (1.0, 2), (0.25, 1), (0.0, 16)])
+def test_hybrid_cpu_gpu(ctx, cutoff, threads):
+    """§8(f)#3 (Alg. 8): GPU from the heavy end of the ExecTime queue, host
+    threads from the light end up to the cut-off — every task exactly once."""
+    import paper_2009_12457_b200 as bb
+    for spec, p in ((("karate", None), 2), (("rmat", 16), 8), (("rmat", 14), 12)):
+        if spec[0] == "karate":
+            s, d = inputs.karate()
+            n = 34
+        else:
+            s, d = inputs.rmat(spec[1], 16, 5)
+            n = 1 << spec[1]
+        og = oracle.OracleGraph(s, d, n)
+        g = bb.Graph.from_edges(ctx, s, d, n)
+        plan = bb.Plan(ctx, g, p)
+        otot, opt, _, _ = og.count(cuts=plan.cuts())
+        with pytest.raises(bb.BBTCError):
+            plan.count_hybrid(threads, cutoff)                      # needs host arenas
+        plan.to_host()
+        plan.stage()
+        tot, pt, st = plan.count_hybrid(threads, cutoff)
+        assert tot == otot and np.array_equal(pt, opt)
+        sparse = plan.n_tasks - plan.info()["dense_tasks"]
+        assert st["cpu_tasks"] + st["gpu_tasks"] == sparse
+        if cutoff == 1.0:
+            assert st["cpu_tasks"] == 0
+        assert st["gpu_tasks"] >= int(np.ceil(cutoff * sparse)) or sparse == 0
+
+
+def test_cut_refinement_and_study_tools(ctx):
+    """§8(f)#4: PBD-like refinement returns valid cuts whose largest block is no larger
+    than the default rule's (and the count is the oracle's); block sizes and per-task
+    times are reported for every task."""
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(16, 16, 2)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    g = bb.Graph.from_edges(ctx, s, d, 1 << 16)
+    for p in (2, 5, 8):
+        base = bb.Plan(ctx, g, p)
+        mm0 = int(base.block_nnz().max())
+        cuts, mm = bb.refine_cuts(ctx, g, p, max_evals=120)
+        assert cuts[0] == 0 and cuts[-1] == og.n and np.all(np.diff(cuts.astype(np.int64)) >= 0)
+        plan = bb.Plan(ctx, g, cuts=cuts)
+        bn = plan.block_nnz()
+        assert int(bn.max()) == mm <= mm0 and int(bn.sum()) == og.m
+        otot, opt, _, _ = og.count(cuts=cuts)
+        tot, pt = plan.count()
+        assert tot == otot and np.array_equal(pt, opt)
+        tt = plan.task_times()
+        assert len(tt) == plan.n_tasks and np.all(tt >= 0) and tt.max() > 0
+    cuts, mm = bb.refine_cuts(ctx, g, 3, cuts=[0, 10, 20, og.n], max_evals=60)
+    assert mm <= int(bb.Plan(ctx, g, cuts=[0, 10, 20, og.n]).block_nnz().max())
