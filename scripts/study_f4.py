@@ -141,6 +141,7 @@ def estim(name, p):
                               else "list + bit rows", "estimator": e, "spearman": spearman(v, times),
                               "coverage_top_x": cov, "mean_coverage": float(np.mean(cov)),
                               "tasks": len(tr), "sum_task_ms": float(times.sum()),
+                              "times_ms": times.tolist(), "estimate": v.tolist(),
                               "top_task_share": float(np.sort(times)[-1] / times.sum())}), flush=True)
         plan.close()
 
