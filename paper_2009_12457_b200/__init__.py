@@ -12,6 +12,7 @@ partition, BCSR, count) runs in the library's sm_100a kernels.
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -83,6 +84,7 @@ class Context:
         L.check(L.bbtc_ctx_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self.device = device
+        self._children = weakref.WeakSet()   # graphs / plans: freed before the context
 
     @property
     def handle(self):
@@ -104,6 +106,8 @@ class Context:
 
     def close(self):
         if getattr(self, "_h", None) and L is not None and L.lib is not None:
+            for c in list(getattr(self, "_children", ())):
+                c.close()
             L.bbtc_ctx_free(self._h)
         self._h = None
 
@@ -117,6 +121,7 @@ class Graph:
     def __init__(self, ctx: Context, h):
         self.ctx = ctx
         self._h = h
+        ctx._children.add(self)
 
     @classmethod
     def from_edges(cls, ctx: Context, src, dst, n_hint: int = 0) -> "Graph":
@@ -208,6 +213,7 @@ class Plan:
                  | (L.PLAN_SPARSE if sparse else 0))
         L.check(L.bbtc_plan_create(ctx.handle, graph._h, p, cptr, flags, ctypes.byref(h)))
         self._h = h
+        ctx._children.add(self)
 
     def info(self) -> dict:
         i = L.bbtc_plan_info()

@@ -306,6 +306,7 @@ def build_sharded(ctx, src, dst, n_hint: int, p: int, cuts=None, group=None, fla
     plan = Plan.__new__(Plan)
     plan.ctx = ctx
     plan._h = hp
+    ctx._children.add(plan)
     mark("build_blocks")
     routes = block_routes(pe, task_rank, block_rank, bnnz_h)
     sent, got = forward_blocks(plan, routes, device, group)

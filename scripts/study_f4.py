@@ -132,6 +132,9 @@ def estim(name, p):
             "Degree": [delta(i, j) + delta(i, k) + delta(j, k) for i, j, k in tr],
             "ExecTime": [bn[bid(i, j)] * max(delta(i, k), delta(j, k)) for i, j, k in tr],
             "ItemCost": [bn[bid(i, j)] * (8 + delta(i, k) + delta(j, k)) for i, j, k in tr],
+            # kernel-aware: probe words per edge, staged list once per column run of G_ij
+            "ProbeCost": [bn[bid(i, j)] * (4 + delta(i, k)) + min(bn[bid(i, j)], sz[j]) * delta(j, k)
+                          for i, j, k in tr],
         }
         for e, v in est.items():
             v = np.asarray(v)
