@@ -92,7 +92,8 @@ typedef struct {
   uint64_t m;               /* unique undirected edges after canonicalisation */
   uint64_t raw_edges;       /* input pairs (incl. self-loops / duplicates) */
   uint32_t d_max;           /* largest full degree d(G,u) in the undirected graph */
-  uint32_t reserved;
+  uint32_t dplus_max;       /* largest out-degree d⁺(u) of the degree-oriented graph;
+                               computed on the first bbtc_graph_stats_get of a graph (one pass) */
 } bbtc_graph_stats;
 
 /* a1-a2.  src/dst: n_edges raw pairs (uint32 each), in host memory (mem ==
@@ -106,6 +107,9 @@ typedef struct {
 BBTC_API bbtc_status bbtc_graph_from_edges(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst,
                                            uint64_t n_edges, uint32_t n_hint, int mem, bbtc_graph** out);
 BBTC_API bbtc_status bbtc_graph_stats_get(const bbtc_graph* g, bbtc_graph_stats* s);
+/* n and m only (host fields, no device work — for hot loops; m of a §8(e) shard = its
+ * own edges). */
+BBTC_API bbtc_status bbtc_graph_size(const bbtc_graph* g, uint32_t* n, uint64_t* m);
 /* rank_of_input_id: host, n entries. */
 BBTC_API bbtc_status bbtc_graph_rank(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t* rank_of_input_id);
 /* The oriented graph in rank space as CSR (row_ptr host n+1, col host m); rows

@@ -145,13 +145,19 @@ class Graph:
         L.check(L.bbtc_graph_stats_get(self._h, ctypes.byref(s)))
         return {f: getattr(s, f) for f, _ in s._fields_ if f != "reserved"}
 
+    def size(self):
+        """(n, m) without device work (bbtc_graph_size)."""
+        n, m = ctypes.c_uint32(), ctypes.c_uint64()
+        L.check(L.bbtc_graph_size(self._h, ctypes.byref(n), ctypes.byref(m)))
+        return int(n.value), int(m.value)
+
     @property
     def n(self) -> int:
-        return self.stats()["n"]
+        return self.size()[0]
 
     @property
     def m(self) -> int:
-        return self.stats()["m"]
+        return self.size()[1]
 
     def rank(self) -> np.ndarray:
         r = np.empty(self.n, np.uint32)

@@ -47,7 +47,7 @@ class bbtc_ctx_opts(ctypes.Structure):
 
 class bbtc_graph_stats(ctypes.Structure):
     _fields_ = [("n", c_u32), ("n_nonisolated", c_u32), ("m", c_u64), ("raw_edges", c_u64), ("d_max", c_u32),
-                ("reserved", c_u32)]
+                ("dplus_max", c_u32)]
 
 
 class bbtc_plan_info(ctypes.Structure):
@@ -97,6 +97,7 @@ bbtc_ctx_stream = _sig("bbtc_ctx_stream", _st, _vp, ctypes.POINTER(_vp))
 bbtc_ctx_launches = _sig("bbtc_ctx_launches", c_u64, _vp)
 bbtc_graph_from_edges = _sig("bbtc_graph_from_edges", _st, _vp, _vp, _vp, c_u64, c_u32, ctypes.c_int, _pp)
 bbtc_graph_stats_get = _sig("bbtc_graph_stats_get", _st, _vp, ctypes.POINTER(bbtc_graph_stats))
+bbtc_graph_size = _sig("bbtc_graph_size", _st, _vp, _u32p, _u64p)
 bbtc_graph_rank = _sig("bbtc_graph_rank", _st, _vp, _vp, _u32p)
 bbtc_graph_csr = _sig("bbtc_graph_csr", _st, _vp, _vp, _u64p, _u32p)
 bbtc_graph_free = _sig("bbtc_graph_free", None, _vp)

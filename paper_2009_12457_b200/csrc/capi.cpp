@@ -694,7 +694,15 @@ BBTC_API bbtc_status bbtc_graph_stats_get(const bbtc_graph* g, bbtc_graph_stats*
     s->m = g->m;
     s->raw_edges = g->raw;
     s->d_max = g->d_max;
-    s->reserved = 0;
+    s->dplus_max = graph_dplus_max(const_cast<bbtc_graph*>(g));
+  });
+}
+
+BBTC_API bbtc_status bbtc_graph_size(const bbtc_graph* g, uint32_t* n, uint64_t* m) {
+  return guard([&] {
+    if (!g || !n || !m) raise(BBTC_EINVAL, "NULL argument");
+    *n = g->n;
+    *m = g->m;
   });
 }
 

@@ -119,6 +119,8 @@ struct bbtc_graph {
   // use 2 m_total); ckeys = the shard's canonical keys (lo << cbw | hi) until ranked.
   uint64_t m_total = 0;
   int cbw = 32;
+  uint32_t dplus_max = 0;             // largest out-degree (on first request, graph_dplus_max)
+  bool dplus_max_known = false;
   bbtc::DevBuf<uint64_t> ckeys;
 };
 
@@ -233,6 +235,7 @@ namespace bbtc {
 void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint,
                  int mem, bbtc_graph* g);
 void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col);
+uint32_t graph_dplus_max(bbtc_graph* g);
 void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,
                 bbtc_plan* plan);
 // count.cu

@@ -154,6 +154,19 @@ __global__ void k_graph_stats(const uint32_t* __restrict__ deg_sorted, uint32_t 
   }
 }
 
+// d⁺(u) = out-degree in the oriented graph (rank space); its maximum (d'_max of the
+// unblocked graph, SURVEY §8(b) stats).
+__global__ void k_outdeg(const uint64_t* __restrict__ okeys, uint64_t m, uint32_t* __restrict__ dplus) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&dplus[(uint32_t)(okeys[e] >> 32)], 1u);
+}
+__global__ void k_max_u32(const uint32_t* __restrict__ x, uint32_t n, uint32_t* __restrict__ out) {
+  uint32_t mx = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) mx = max(mx, x[i]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
 // ---- a3 ------------------------------------------------------------------------------
 struct ToU64 {
   __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
@@ -799,6 +812,30 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     g->n_nonisolated = n - h[0];
     g->d_max = h[1];
   }
+}
+
+// Largest out-degree of the oriented graph (computed on first request, cached).
+uint32_t graph_dplus_max(bbtc_graph* g) {
+  if (g->dplus_max_known) return g->dplus_max;
+  bbtc_ctx* ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  uint32_t mx = 0;
+  if (g->n && g->m && g->okeys.p) {
+    DevBuf<uint32_t> dp, out;
+    dp.alloc(g->n, ctx);
+    out.alloc(1, ctx);
+    BBTC_CUDA(cudaMemsetAsync(dp.p, 0, (size_t)g->n * 4, st));
+    BBTC_CUDA(cudaMemsetAsync(out.p, 0, 4, st));
+    k_outdeg<<<grid_for(ctx, g->m), kThreads, 0, st>>>(g->okeys.p, g->m, dp.p);
+    BBTC_LAUNCHED(ctx);
+    k_max_u32<<<grid_for(ctx, g->n), kThreads, 0, st>>>(dp.p, g->n, out.p);
+    BBTC_LAUNCHED(ctx);
+    BBTC_CUDA(cudaMemcpyAsync(&mx, out.p, 4, cudaMemcpyDeviceToHost, st));
+    BBTC_CUDA(cudaStreamSynchronize(st));
+  }
+  g->dplus_max = mx;
+  g->dplus_max_known = true;
+  return mx;
 }
 
 void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col) {

@@ -265,7 +265,7 @@ def build_sharded(ctx, src, dst, n_hint: int, p: int, cuts=None, group=None, fla
                                ctypes.c_void_p(deg.data_ptr()), ctypes.byref(h)))
     g = Graph(ctx, h)
     del recv
-    m_local = g.stats()["m"]
+    m_local = g.m
     mt = torch.tensor([m_local], dtype=torch.int64, device=device)
     _all_reduce(mt, dist.ReduceOp.SUM, group)
     _all_reduce(deg, dist.ReduceOp.SUM, group)

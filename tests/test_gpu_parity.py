@@ -78,6 +78,8 @@ def test_rmat16_preprocessing_matches_oracle(ctx):
     row, col = g.csr()
     orow, ocol = og.csr()
     assert np.array_equal(row, orow) and np.array_equal(col, ocol)
+    assert st["dplus_max"] == int(np.diff(orow.astype(np.int64)).max())   # d+_max
+    assert g.size() == (og.n, og.m)
 
 
 def test_blocks_round_trip(ctx):
