@@ -422,12 +422,12 @@ struct Streamer {
   // Column offsets a streamed copy of block b carries (0 unless ccv travels as colptr).
   uint64_t clen(uint32_t b) const {
     const BlockDesc& B = plan->blocks[b];
-    return plan->streams_colptr() && B.nnz ? (uint64_t)B.nc + 1 : 0;
+    return plan->block_colptr(b) && B.nnz ? (uint64_t)B.nc + 1 : 0;
   }
   // Device bytes of block b's streamed form (per-edge arenas + row and column offsets).
   uint64_t block_bytes(uint32_t b) const {
     const BlockDesc& B = plan->blocks[b];
-    return 4 * B.nnz * plan->stream_edge_arenas() + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1) +
+    return 4 * B.nnz * plan->stream_edge_arenas(b) + 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1) +
            4 * clen(b);
   }
   // Copies block b from the pinned host arenas to device arenas (edge arrays at
@@ -443,7 +443,7 @@ struct Streamer {
     cudaStream_t cs = ctx->copy_streams[rr++ % ctx->copy_streams.size()];
     const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
     auto arenas = plan->edge_arenas();
-    const size_t direct = plan->stream_edge_arenas();   // colptr form: arena 2 (ccv) stays home
+    const size_t direct = plan->stream_edge_arenas(b);   // colptr form: arena 2 (ccv) stays home
     if (B.nnz)
       for (size_t x = 0; x < direct; ++x)
         BBTC_CUDA(cudaMemcpyAsync(dev_edges[x] + e_dst, *arenas[x].host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
@@ -825,7 +825,8 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     for (size_t b = 0; b < plan->blocks.size(); ++b) {
       const BlockDesc& B = plan->blocks[b];
       plan->info.stream_bytes += 4 * ((uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1 - plan->rp_zero[b]);
-      if (plan->colmajor && B.nnz) plan->info.stream_bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.j + 1] - plan->cuts[B.j]) + 1);
+      if (plan->block_colptr((uint32_t)b) && B.nnz)
+        plan->info.stream_bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[B.j + 1] - plan->cuts[B.j]) + 1);
       else plan->info.stream_bytes += 4 * B.nnz * plan->edge_arenas().size();
     }
     BBTC_CUDA(cudaStreamSynchronize(st));
@@ -1046,24 +1047,27 @@ static void stream_order(bbtc_ctx* ctx, bbtc_plan* plan) {
   plan->s_ready = true;
 }
 
+// A/B knob (BBTC_FORCE_CP=1): the streamed walk (column offsets, kCP) over resident
+// blocks of a host plan that kept its device column offsets; else NULL (the plan's arenas).
+static const DevArenas* ab_colptr_arenas(bbtc_plan* plan, DevArenas* ar) {
+  if (!(getenv("BBTC_FORCE_CP") && plan->d_colptr.p && plan->d_item_col.p)) return nullptr;
+  ar->cols = plan->cols.p;
+  ar->it_u = plan->ccu.p;
+  ar->it_v = plan->ccv.p;
+  ar->rowptr = plan->rowptr.p;
+  ar->blocks = plan->d_blocks.p;
+  ar->colptr = plan->d_colptr.p;
+  ar->item_col = plan->d_item_col.p;
+  return ar;
+}
+
 // Resident blocks: the list kernel over the sparse tasks' items, then the bit-row
 // kernel over the dense tasks' items (building the bit rows on first use).
 static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                            cudaEvent_t mid = nullptr) {
   dense_build(ctx, plan);
-  if (getenv("BBTC_FORCE_CP") && plan->d_colptr.p && plan->d_item_col.p) {
-    // A/B: the streamed walk (column offsets, kCP) over resident blocks
-    DevArenas ar;
-    ar.cols = plan->cols.p;
-    ar.it_u = plan->ccu.p;
-    ar.rowptr = plan->rowptr.p;
-    ar.blocks = plan->d_blocks.p;
-    ar.colptr = plan->d_colptr.p;
-    ar.item_col = plan->d_item_col.p;
-    count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0, &ar);
-  } else {
-    count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0);
-  }
+  DevArenas ar;
+  count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0, ab_colptr_arenas(plan, &ar));
   if (mid) BBTC_CUDA(cudaEventRecord(mid, ctx->stream));
   count_launch_dense(ctx, plan, rank, world, d_counts, plan->dense_item_lo, plan->item_start.back());
 }
@@ -1112,7 +1116,8 @@ BBTC_API bbtc_status bbtc_task_times(bbtc_ctx* ctx, const bbtc_plan* cplan, doub
       const uint64_t lo = plan->item_start[t], hi = plan->item_start[t + 1];
       BBTC_CUDA(cudaEventRecord(a, ctx->stream));
       if (hi > lo) {
-        if (t < plan->dense_task_lo) count_launch(ctx, plan, 0, 1, d_counts.p, lo, hi, nullptr, 0);
+        DevArenas ar;
+        if (t < plan->dense_task_lo) count_launch(ctx, plan, 0, 1, d_counts.p, lo, hi, nullptr, 0, ab_colptr_arenas(plan, &ar));
         else count_launch_dense(ctx, plan, 0, 1, d_counts.p, lo, hi);
       }
       BBTC_CUDA(cudaEventRecord(b, ctx->stream));
@@ -1459,7 +1464,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       DevArenas full;
       full.cols = plan->cols.p;
       full.it_u = plan->colmajor ? plan->ccu.p : plan->rows.p;
-      full.it_v = plan->colmajor ? (plan->streams_colptr() ? nullptr : plan->ccv.p) : plan->cols.p;
+      full.it_v = plan->colmajor ? plan->ccv.p : plan->cols.p;   // (kCP: the ccv-shipping blocks)
       full.rowptr = plan->rowptr.p;
       full.blocks = plan->d_blocks.p;
       full.colptr = plan->streams_colptr() ? plan->d_colptr.p : nullptr;
@@ -1486,8 +1491,9 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
       // ones are copied into free cache space (first fit), every block of the window
       // is flagged with the window's epoch, and the count kernel runs over the
       // window's work items, its warps waiting on the flags as in the streamed mode.
-      const uint64_t A = plan->stream_edge_arenas();
       const bool cpf = plan->streams_colptr();
+      uint64_t A = 2;   // edge arenas of the cache: 3 when some block ships its column ids
+      for (uint32_t b = 0; b < plan->blocks.size(); ++b) A = std::max<uint64_t>(A, plan->stream_edge_arenas(b));
       Streamer sz(ctx, plan);
       uint64_t ro_all = 0;   // row offsets + (colptr form) column offsets of every block
       for (uint32_t b = 0; b < plan->blocks.size(); ++b)
@@ -1623,7 +1629,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         for (uint32_t b : wblocks) {
           tab[b].e0 = (uint64_t)at_e[b];
           tab[b].ro = (uint64_t)at_r[b];
-          tab[b].co = (uint64_t)at_r[b] + rowlen(b);
+          if (tab[b].co != kNoColptr) tab[b].co = (uint64_t)at_r[b] + rowlen(b);
         }
         tables.emplace_back();
         tables.back().alloc(nb, ctx);
@@ -1640,7 +1646,7 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* cplan, uint32_t 
         DevArenas ar;
         ar.cols = dev_edges[0];
         ar.it_u = dev_edges[1];
-        ar.it_v = plan->colmajor ? (cpf ? nullptr : dev_edges[2]) : dev_edges[0];
+        ar.it_v = plan->colmajor ? dev_edges[2] : dev_edges[0];   // (kCP: the ccv-shipping blocks)
         ar.rowptr = cache_rp.p;
         ar.blocks = tables.back().p;
         ar.colptr = cpf ? cache_rp.p : nullptr;

@@ -310,9 +310,11 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     const uint32_t* rpS = rowptr + BS.ro;
     const uint32_t* cS = cols + BS.e0;
     const uint32_t* rpP = rowptr + BP.ro;
-    const uint32_t* cpb = kCP ? colptr + Bij.co : nullptr;   // G_ij's column offsets (kCP)
+    // kCP: G_ij's column offsets, unless the block ships its column ids (kNoColptr)
+    const bool cpm = kCP && Bij.co != kNoColptr;
+    const uint32_t* cpb = cpm ? colptr + Bij.co : nullptr;
     uint32_t ccol = 0;                                        // a column with cpb[ccol] <= next edge
-    if constexpr (kCP) ccol = item_col[T.icol + (g - item_start[lo])];   // (k_item_cols, plan time)
+    if (cpm) ccol = item_col[T.icol + (g - item_start[lo])];  // (k_item_cols, plan time)
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
@@ -322,7 +324,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const bool valid = e < e_end;
       const uint32_t u = valid ? it_u[e] : 0xFFFFFFFFu;
       uint32_t v;
-      if constexpr (kCP) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
+      if (cpm) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
       else v = valid ? it_v[e] : 0xFFFFFFFFu;
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
@@ -378,8 +380,8 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         if (L == 32 && __all_sync(kFull, valid && key == k0)) {
           // kCP: the run's edges end where column k0 ends
-          const uint64_t run_end = kCP ? Bij.e0 + cpb[k0 + 1] : 0;
-          auto same = [&](uint64_t e) { return kCP ? e < run_end : (kCol ? it_v[e] : it_u[e]) == k0; };
+          const uint64_t run_end = cpm ? Bij.e0 + cpb[k0 + 1] : 0;
+          auto same = [&](uint64_t e) { return cpm ? e < run_end : (kCol ? it_v[e] : it_u[e]) == k0; };
           if constexpr (kRunPipe && (!kBm || BBTC_RUN_PIPE_BM)) {
             // Two-stage pipeline over the run's batches: while batch t is probed, the row
             // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
@@ -486,7 +488,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       }
       // kCP: the next batch starts after the last consumed edge, in its column or later
       // (a continued run consumed only edges of column k0 = lane 31's column)
-      if constexpr (kCP) ccol = __shfl_sync(kFull, v, min(L, 32) - 1);
+      if (cpm) ccol = __shfl_sync(kFull, v, min(L, 32) - 1);
       base += L;
     }
     // one atomic pair per warp-item

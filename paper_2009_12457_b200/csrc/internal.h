@@ -126,12 +126,14 @@ struct bbtc_graph {
 
 // One upper-triangular block G_ij in the arena (column-major block order:
 // b = j(j+1)/2 + i).
+constexpr uint64_t kNoColptr = ~0ull;   // BlockDesc.co of a block streamed with per-edge column ids
 struct BlockDesc {
   uint64_t e0;      // first edge (index into cols / rows arenas)
   uint64_t nnz;     // edges
   uint64_t ro;      // first row offset (index into rowptr arena); |V_i|+1 entries
   uint32_t i, j;
-  uint64_t co;      // streamed column-major blocks: first of its |V_j|+1 column offsets (colptr arena)
+  uint64_t co;      // streamed column-major blocks: first of its |V_j|+1 column offsets (colptr arena),
+                    // kNoColptr when the block streams its per-edge column ids (nnz <= |V_j|+1)
   uint32_t nc;      // columns |V_j|
   uint32_t pad_;
 };
@@ -227,7 +229,9 @@ struct bbtc_plan {
   // The per-edge arenas a streamed copy moves: a column-major block's ccv travels as
   // column offsets (colptr), so only cols + ccu cross per edge.
   bool streams_colptr() const { return colmajor && h_colptr != nullptr; }
-  size_t stream_edge_arenas() const { return colmajor ? (h_colptr ? 2 : 3) : 2; }
+  // per block: column offsets (fewer words than nnz column ids) or the ids themselves
+  bool block_colptr(uint32_t b) const { return streams_colptr() && blocks[b].co != kNoColptr; }
+  size_t stream_edge_arenas(uint32_t b) const { return colmajor ? (block_colptr(b) ? 2 : 3) : 2; }
 };
 
 namespace bbtc {

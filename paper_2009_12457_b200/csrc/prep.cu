@@ -377,6 +377,7 @@ __global__ void k_col_starts(const uint32_t* __restrict__ ccv, const BlockDesc* 
                              uint32_t* __restrict__ colptr) {
   for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
     const BlockDesc B = blocks[b];
+    if (co[b] == kNoColptr) continue;
     uint32_t* C = colptr + co[b];
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < B.nnz;
          x += (uint64_t)gridDim.x * blockDim.x) {
@@ -390,6 +391,7 @@ __global__ void k_col_local(const BlockDesc* __restrict__ blocks, const uint64_t
                             const uint32_t* __restrict__ cuts, uint32_t* __restrict__ colptr) {
   for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
     const BlockDesc B = blocks[b];
+    if (co[b] == kNoColptr) continue;
     const uint32_t len = cuts[B.j + 1] - cuts[B.j] + 1;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < len; c += gridDim.x * blockDim.x)
       colptr[co[b] + c] -= (uint32_t)B.e0;
@@ -409,6 +411,10 @@ __global__ void k_item_cols(const TaskDesc* __restrict__ tasks, const uint64_t* 
       if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const TaskDesc T = tasks[lo];
+    if (co[T.ij] == kNoColptr) {   // (the block streams its column ids)
+      item_col[T.icol + (g - item_start[lo])] = 0;
+      continue;
+    }
     const uint64_t x = (g - item_start[lo]) * T.chunk;   // local offset of the item's first edge
     const uint32_t* cp = colptr + co[T.ij];
     uint32_t a = 0, b = blocks[T.ij].nc - 1;               // largest c with cp[c] <= x
@@ -428,7 +434,7 @@ __global__ void k_col_expand_all(const uint32_t* __restrict__ colptr, const Bloc
   const int lane = threadIdx.x & 31;
   for (uint32_t b = blockIdx.y; b < nb; b += gridDim.y) {
     const BlockDesc B = blocks[b];
-    if (!B.nnz) continue;
+    if (!B.nnz || B.co == kNoColptr) continue;   // (ccv copied as it is)
     const uint32_t* C = colptr + B.co;
     uint32_t* V = ccv + B.e0;
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
@@ -1101,13 +1107,21 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
 uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
   cudaStream_t st = ctx->stream;
   const uint32_t nb = (uint32_t)plan->blocks.size();
+  // A block streams column offsets (|V_j|+1 words) only where that is fewer words
+  // than its per-edge column ids (nnz): blocks with mostly empty columns (rmat24's
+  // (0,0): 15 M columns, 1.5 M edges) ship ccv itself, and the kernel reads it.
   plan->co_off.assign(nb + 1, 0);
+  std::vector<uint64_t> co(nb + 1, kNoColptr);
   uint32_t maxw = 1;
   for (uint32_t b = 0; b < nb; ++b) {
     const BlockDesc& B = plan->blocks[b];
     const uint32_t w = plan->cuts[B.j + 1] - plan->cuts[B.j];
-    maxw = std::max(maxw, w + 1);
-    plan->co_off[b + 1] = plan->co_off[b] + w + 1;
+    const bool cp = B.nnz > (uint64_t)w + 1;
+    if (cp) {
+      maxw = std::max(maxw, w + 1);
+      co[b] = plan->co_off[b];
+    }
+    plan->co_off[b + 1] = plan->co_off[b] + (cp ? w + 1 : 0);
   }
   const uint64_t len = plan->co_off[nb];
   out->alloc(std::max<uint64_t>(len, 1), ctx);
@@ -1115,7 +1129,7 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
   DevBuf<uint32_t> dcuts;
   dco.alloc(nb + 1, ctx);
   dcuts.alloc(plan->cuts.size(), ctx);
-  BBTC_CUDA(cudaMemcpyAsync(dco.p, plan->co_off.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
+  BBTC_CUDA(cudaMemcpyAsync(dco.p, co.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaMemcpyAsync(dcuts.p, plan->cuts.data(), plan->cuts.size() * 4, cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaMemsetAsync(out->p, 0xFF, len * 4, st));
   if (nb) {
@@ -1138,8 +1152,8 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
       BBTC_LAUNCHED(ctx);
     }
   }
-  // the streamed kernel finds block b's column offsets at co (BlockDesc.co)
-  for (uint32_t b = 0; b < nb; ++b) plan->blocks[b].co = plan->co_off[b];
+  // the streamed kernel finds block b's column offsets at co (BlockDesc.co; kNoColptr: ccv)
+  for (uint32_t b = 0; b < nb; ++b) plan->blocks[b].co = co[b];
   BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaStreamSynchronize(st));   // dco / dcuts die with this scope
   return len;
