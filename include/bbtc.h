@@ -284,11 +284,11 @@ BBTC_API bbtc_status bbtc_count(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t r
                                 uint32_t flags, uint64_t* total, uint64_t* per_task, bbtc_timing* t);
 
 /* §8(f)#4 study support.  bbtc_plan_block_nnz: nnz of every block, HOST uint64[p(p+1)/2]
- * (block order b = j(j+1)/2 + i).  bbtc_task_times: device time of every task alone
- * (HOST double[n_tasks], canonical order, milliseconds; CUDA events around one launch of
- * the task's own work items — list or bit-row kernel), for ranking workload estimators
- * against measured task times.  Needs resident blocks.  Slow (one launch
- * per task): a study tool, not a counting path. */
+ * (block order b = j(j+1)/2 + i).  bbtc_task_times: the warp time every task took
+ * inside one ordinary resident count (HOST double[n_tasks], canonical order, warp-
+ * milliseconds = Σ over the task's work items of the item's clock64() span / SM clock),
+ * for ranking workload estimators against measured task work.  Needs
+ * resident blocks.  A study tool: the instrumented count is otherwise the real one. */
 BBTC_API bbtc_status bbtc_plan_block_nnz(const bbtc_plan* plan, uint64_t* nnz);
 BBTC_API bbtc_status bbtc_task_times(bbtc_ctx* ctx, const bbtc_plan* plan, double* ms);
 /* A PBD-like refinement of a cut vector (P:459-460 cite PBD without describing it; SPEC's

@@ -1104,30 +1104,28 @@ BBTC_API bbtc_status bbtc_task_times(bbtc_ctx* ctx, const bbtc_plan* cplan, doub
     if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident");
     BBTC_CUDA(cudaSetDevice(ctx->device));
     const uint64_t nt = plan->info.n_tasks;
-    std::fill(ms, ms + nt, 0.0);
-    DevBuf<uint64_t> d_counts;
+    DevBuf<uint64_t> d_counts, cyc;
     d_counts.alloc(nt + 1, ctx);
+    cyc.alloc(nt, ctx);
+    BBTC_CUDA(cudaMemsetAsync(cyc.p, 0, nt * 8, ctx->stream));
     count_zero(ctx, plan, d_counts.p);
-    dense_build(ctx, plan);
-    cudaEvent_t a, b;
-    BBTC_CUDA(cudaEventCreate(&a));
-    BBTC_CUDA(cudaEventCreate(&b));
-    for (size_t t = 0; t < plan->tasks.size(); ++t) {
-      const uint64_t lo = plan->item_start[t], hi = plan->item_start[t + 1];
-      BBTC_CUDA(cudaEventRecord(a, ctx->stream));
-      if (hi > lo) {
-        DevArenas ar;
-        if (t < plan->dense_task_lo) count_launch(ctx, plan, 0, 1, d_counts.p, lo, hi, nullptr, 0, ab_colptr_arenas(plan, &ar));
-        else count_launch_dense(ctx, plan, 0, 1, d_counts.p, lo, hi);
-      }
-      BBTC_CUDA(cudaEventRecord(b, ctx->stream));
-      BBTC_CUDA(cudaEventSynchronize(b));
-      float f = 0;
-      BBTC_CUDA(cudaEventElapsedTime(&f, a, b));
-      ms[plan->tasks[t].idx] = f;
+    // One ordinary resident count whose warps add each work item's clock64() span to
+    // its task: the task's total warp time inside the real launch (one launch per task
+    // would time the latency of its longest item instead).
+    ctx->task_cycles = cyc.p;
+    try {
+      count_resident(ctx, plan, 0, 1, d_counts.p);
+    } catch (...) {
+      ctx->task_cycles = nullptr;
+      throw;
     }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    ctx->task_cycles = nullptr;
+    std::vector<uint64_t> h(nt);
+    BBTC_CUDA(cudaMemcpyAsync(h.data(), cyc.p, nt * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
+    int khz = 0;
+    BBTC_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device));
+    for (uint64_t t = 0; t < nt; ++t) ms[t] = (double)h[t] / std::max(khz, 1);
   });
 }
 

@@ -30,7 +30,8 @@ constexpr int kHashCap = kLoadHalf ? kTable / 2 : kTable / 4;   // staged words 
 constexpr int kChunk = kTable / 2;   // staged words of a single-list table fill (load <= 1/2)
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr size_t kSmemBytes = (size_t)kWarps * (kTable * 4 + 32 * 16);
+constexpr size_t kSmemBytes = (size_t)kWarps * (kTable * 4 + 32 * 16);   // table + payload (uint2[32]) + spare
+static_assert(32 * 16 >= 32 * 8 + 8, "the payload area's spare half holds a warp's study-mode clock");
 constexpr int kCtasPerSm = 8;        // cap on resident CTAs per SM (BBTC_CTAS_PER_SM overrides)
 #ifndef BBTC_MIN_CTAS
 #define BBTC_MIN_CTAS 5
@@ -262,7 +263,8 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
         unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch,
-        const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ item_col) {
+        const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ item_col,
+        unsigned long long* __restrict__ task_cycles) {
   static_assert(!kCP || kCol, "column offsets replace the column ids of a column-major walk");
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -277,6 +279,12 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     it = __shfl_sync(kFull, it, 0);
     const uint64_t g = item_lo + it * world + rank;
     if (g >= n_items) break;
+    // study mode (bbtc_task_times): the item's start clock in the spare half of the warp's
+    // payload area (shared memory, so the main loop carries no extra live register)
+    auto t_slot = [&]() {
+      return reinterpret_cast<long long*>(reinterpret_cast<uint2*>(smem + kWarps * kTable) + kWarps * 32) + wid;
+    };
+    if (task_cycles && lane == 0) *t_slot() = clock64();
     // task of item g: last t with item_start[t] <= g
     uint32_t lo = 0, hi = n_exec - 1;
     while (lo < hi) {
@@ -497,6 +505,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       atomicAdd(&counts[T.idx], (unsigned long long)s);
       atomicAdd(&counts[n_tasks], (unsigned long long)s);
     }
+    if (task_cycles && lane == 0) atomicAdd(&task_cycles[T.idx], (unsigned long long)(clock64() - *t_slot()));
   }
 }
 
@@ -586,7 +595,8 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
               const BlockDesc* __restrict__ blocks, const TaskDesc* __restrict__ tasks,
               const uint64_t* __restrict__ item_start, uint32_t n_exec, uint64_t item_lo, uint64_t n_items,
               uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
-              unsigned long long* __restrict__ counts, uint32_t n_tasks) {
+              unsigned long long* __restrict__ counts, uint32_t n_tasks,
+              unsigned long long* __restrict__ task_cycles) {
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long it = 0;
@@ -594,6 +604,7 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
     it = __shfl_sync(kFull, it, 0);
     const uint64_t g = item_lo + it * world + rank;
     if (g >= n_items) break;
+    const long long t_item = task_cycles ? clock64() : 0;
     uint32_t lo = 0, hi = n_exec - 1;
     while (lo < hi) {
       uint32_t mid = (lo + hi + 1) >> 1;
@@ -620,6 +631,7 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
       atomicAdd(&counts[T.idx], (unsigned long long)s);
       atomicAdd(&counts[n_tasks], (unsigned long long)s);
     }
+    if (task_cycles && lane == 0) atomicAdd(&task_cycles[T.idx], (unsigned long long)(clock64() - t_item));
   }
 }
 
@@ -699,7 +711,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
                          const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
                          unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t,
-                         const uint32_t*, const uint32_t*);
+                         const uint32_t*, const uint32_t*, unsigned long long*);
   // The bitmap variant only where some task's V_k is small enough (it costs the main
   // loop a few registers: friendster, whose parts are all large, measured 0.7% slower).
   bool bm = false;
@@ -748,7 +760,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
       n_exec ? n_exec : (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
-      (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col);
+      (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col, (unsigned long long*)ctx->task_cycles);
   BBTC_LAUNCHED(ctx);
 }
 
@@ -810,7 +822,8 @@ void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uin
   k_count_dense<<<(unsigned)grid, kWarps * 32, 0, st>>>(
       plan->colmajor ? plan->ccu.p : plan->rows.p, plan->colmajor ? plan->ccv.p : plan->cols.p, plan->dense.p,
       plan->d_dense_off.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p, (uint32_t)plan->tasks.size(),
-      item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts, (uint32_t)plan->info.n_tasks);
+      item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts, (uint32_t)plan->info.n_tasks,
+      (unsigned long long*)ctx->task_cycles);
   BBTC_LAUNCHED(ctx);
 }
 

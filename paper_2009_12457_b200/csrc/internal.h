@@ -94,6 +94,7 @@ struct bbtc_ctx {
   int sm_count = 148;
   void* cursor = nullptr;          // device scratch: work-item cursors of the count kernel
   uint64_t cursor_next = 0;
+  uint64_t* task_cycles = nullptr;   // study mode (bbtc_task_times): per-task warp cycles, else NULL
   std::multimap<size_t, void*> cache;   // caching allocator: size class -> free blocks
   size_t cached_bytes = 0;
   size_t cache_limit = 0;

@@ -1116,7 +1116,10 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
   for (uint32_t b = 0; b < nb; ++b) {
     const BlockDesc& B = plan->blocks[b];
     const uint32_t w = plan->cuts[B.j + 1] - plan->cuts[B.j];
-    const bool cp = B.nnz > (uint64_t)w + 1;
+    // (>= 4 edges per column on average: with sparser columns the kernel's 32-column
+    // windows cover too few edges per batch — rmat24 (1,1): 2 edges/column, the
+    // column-offset walk 2.7x slower than reading ccv, scripts/dbg_cp_tasks.py)
+    const bool cp = B.nnz >= 4 * ((uint64_t)w + 1);
     if (cp) {
       maxw = std::max(maxw, w + 1);
       co[b] = plan->co_off[b];
