@@ -473,6 +473,94 @@ __global__ void k_low_bits(const K* __restrict__ keys, uint64_t m, int cb, uint3
     out[e] = (uint32_t)(keys[e] & mask);
 }
 
+// ---- a1 bucket sort: canonical keys de-duplicated in hashed buckets -----------------
+// The K-bit keys (lo << bw | hi) are mixed by an odd multiplier mod 2^K (a bijection),
+// split into 2^BB buckets by the top BB mixed bits, and each bucket (<= kBktCap keys,
+// the remaining R = K - BB <= 32 bits as a u32) is sorted and de-duplicated in shared
+// memory by one CTA; survivors are unmixed back into keys.  Equal keys meet in one
+// bucket, so the unique set is exact; its order is arbitrary (nothing downstream needs
+// one: degrees use atomics, orientation is per key, the block sort orders the edges).
+constexpr int kBktThreads = 256, kBktItems = 16, kBktCap = kBktThreads * kBktItems;
+struct BktMix {
+  uint64_t c, cinv, kmask;
+  int K, R;
+  __host__ __device__ uint64_t mix(uint64_t k) const { return (k * c) & kmask; }
+  __host__ __device__ uint64_t unmix(uint64_t x) const { return (x * cinv) & kmask; }
+};
+__global__ void k_bkt_count(const uint64_t* __restrict__ keys, uint64_t E, BktMix mx,
+                            uint32_t* __restrict__ counts) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    if (k != kSentinel) atomicAdd(&counts[mx.mix(k) >> mx.R], 1u);
+  }
+}
+__global__ void k_bkt_scatter(const uint64_t* __restrict__ keys, uint64_t E, BktMix mx, uint32_t* __restrict__ cursor,
+                              uint32_t* __restrict__ out) {
+  const uint32_t rmask = mx.R >= 32 ? 0xFFFFFFFFu : ((1u << mx.R) - 1);
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[e];
+    if (k == kSentinel) continue;
+    const uint64_t x = mx.mix(k);
+    out[atomicAdd(&cursor[x >> mx.R], 1u)] = (uint32_t)x & rmask;
+  }
+}
+// One CTA per bucket: sort its keys in shared memory, keep the first of every run of
+// equal keys (in place, at the front of the bucket), count them.
+__global__ void __launch_bounds__(kBktThreads) k_bkt_sort(uint32_t* __restrict__ data, const uint32_t* __restrict__ offs,
+                                                          const uint32_t* __restrict__ counts, int R,
+                                                          uint32_t* __restrict__ ucount) {
+  using Sort = cub::BlockRadixSort<uint32_t, kBktThreads, kBktItems>;
+  using Scan = cub::BlockScan<uint32_t, kBktThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_last[kBktThreads];
+  const uint32_t b = blockIdx.x;
+  const uint32_t n = counts[b];
+  if (n == 0) {
+    if (threadIdx.x == 0) ucount[b] = 0;
+    return;
+  }
+  uint32_t* d = data + offs[b];
+  uint32_t k[kBktItems];
+#pragma unroll
+  for (int x = 0; x < kBktItems; ++x) {
+    const uint32_t i = threadIdx.x * kBktItems + x;   // blocked: thread t holds [16t, 16t+16)
+    k[x] = i < n ? d[i] : 0xFFFFFFFFu;                 // padding sorts last
+  }
+  Sort(tmp.sort).Sort(k, 0, R);
+  __syncthreads();
+  s_last[threadIdx.x] = k[kBktItems - 1];
+  __syncthreads();
+  uint32_t keep[kBktItems], total = 0;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int x = 0; x < kBktItems; ++x) {
+    const uint32_t i = threadIdx.x * kBktItems + x;
+    const uint32_t prev = x ? k[x - 1] : (threadIdx.x ? s_last[threadIdx.x - 1] : 0);
+    keep[x] = i < n && (i == 0 || k[x] != prev);
+    mine += keep[x];
+  }
+  uint32_t at = 0;
+  Scan(tmp.scan).ExclusiveSum(mine, at, total);
+  __syncthreads();   // every key was read before any is written
+#pragma unroll
+  for (int x = 0; x < kBktItems; ++x)
+    if (keep[x]) d[at++] = k[x];
+  if (threadIdx.x == 0) ucount[b] = total;
+}
+// Survivors of bucket b -> unmixed keys at uoffs[b].
+__global__ void k_bkt_compact(const uint32_t* __restrict__ data, const uint32_t* __restrict__ offs,
+                              const uint32_t* __restrict__ ucount, const uint32_t* __restrict__ uoffs, uint32_t nb,
+                              BktMix mx, uint64_t* __restrict__ ukeys) {
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint32_t n = ucount[b], o = offs[b], u = uoffs[b];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+      ukeys[u + i] = mx.unmix(((uint64_t)b << mx.R) | data[o + i]);
+  }
+}
+
 // ---- §8(e) sharded build: grouping keys by destination rank -----------------------
 // Owner rank of a canonical edge (lo << 32 | hi): a hash of its lower id, so every
 // instance of an edge (from any rank's raw shard) meets at one rank.
@@ -557,6 +645,61 @@ __global__ void k_narrow(uint64_t* __restrict__ keys, uint64_t m, int bw) {
 }
 
 }  // namespace
+
+// a1 bucket de-duplication of keys[0, E) (K live bits; sentinels skipped).  Returns
+// false (nothing done) when it does not apply: a bucket above kBktCap keys (heavy
+// duplication of one edge) or sizes outside its range — the caller sorts instead.
+static bool bucket_unique(bbtc_ctx* ctx, const uint64_t* keys, uint64_t E, int K, DevBuf<uint64_t>* ukeys,
+                          uint64_t* m_out) {
+  cudaStream_t st = ctx->stream;
+  if (E < (1ull << 22) || E >= (1ull << 32) || K < 36 || K > 56) return false;
+  int BB = std::max(K - 32, bitlen(E / 2048));
+  if (BB > 22 || BB >= K) return false;
+  BktMix mx;
+  mx.K = K;
+  mx.R = K - BB;
+  mx.kmask = K >= 64 ? ~0ull : ((1ull << K) - 1);
+  mx.c = 0x9E3779B97F4A7C15ull;   // odd: x -> c*x is a bijection mod 2^K
+  uint64_t inv = mx.c;            // Newton: inv = c^-1 mod 2^64
+  for (int it = 0; it < 6; ++it) inv *= 2 - mx.c * inv;
+  mx.cinv = inv;
+  const uint32_t nb = 1u << BB;
+  DevBuf<uint32_t> counts, offs, cursor, ucount, uoffs, data, mx_d;
+  counts.alloc(nb, ctx);
+  offs.alloc(nb, ctx);
+  mx_d.alloc(1, ctx);
+  BBTC_CUDA(cudaMemsetAsync(counts.p, 0, nb * 4, st));
+  k_bkt_count<<<grid_for(ctx, E), kThreads, 0, st>>>(keys, E, mx, counts.p);
+  BBTC_LAUNCHED(ctx);
+  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, counts.p, mx_d.p, nb, st); });
+  uint32_t biggest = 0;
+  BBTC_CUDA(cudaMemcpyAsync(&biggest, mx_d.p, 4, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  if (biggest > (uint32_t)kBktCap) return false;
+  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, counts.p, offs.p, nb, st); });
+  cursor.alloc(nb, ctx);
+  BBTC_CUDA(cudaMemcpyAsync(cursor.p, offs.p, nb * 4, cudaMemcpyDeviceToDevice, st));
+  data.alloc(E, ctx);
+  k_bkt_scatter<<<grid_for(ctx, E), kThreads, 0, st>>>(keys, E, mx, cursor.p, data.p);
+  BBTC_LAUNCHED(ctx);
+  cursor.reset();
+  ucount.alloc(nb, ctx);
+  k_bkt_sort<<<nb, kBktThreads, 0, st>>>(data.p, offs.p, counts.p, mx.R, ucount.p);
+  BBTC_LAUNCHED(ctx);
+  uoffs.alloc(nb, ctx);
+  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, ucount.p, uoffs.p, nb, st); });
+  uint32_t last[2] = {0, 0};
+  BBTC_CUDA(cudaMemcpyAsync(&last[0], uoffs.p + nb - 1, 4, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaMemcpyAsync(&last[1], ucount.p + nb - 1, 4, cudaMemcpyDeviceToHost, st));
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  const uint64_t m = (uint64_t)last[0] + last[1];
+  ukeys->alloc(std::max<uint64_t>(m, 1), ctx);
+  k_bkt_compact<<<std::min<uint32_t>(nb, (uint32_t)ctx->sm_count * 16), kThreads, 0, st>>>(
+      data.p, offs.p, ucount.p, uoffs.p, nb, mx, ukeys->p);
+  BBTC_LAUNCHED(ctx);
+  *m_out = m;
+  return true;
+}
 
 // =====================================================================================
 void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint, int mem,
@@ -691,6 +834,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   // Sort the canonical keys over their live bits (hi id in [0,bid), lo id in [bw,bw+bid)).
   uint64_t m = 0;
   DevBuf<uint64_t> ukeys;
+  bool unsorted = use_hash;   // unique keys in no particular order (hash set / buckets)
   if (E && use_hash) {
     // The set's occupied slots are the unique edges (in no particular order).
     const uint64_t T = 1ull << tbits;
@@ -746,6 +890,9 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       }
       in_keys = sel == 0;
       sort_tmp.reset();
+    } else if (!getenv("BBTC_NO_BUCKET") && bucket_unique(ctx, keys.p, E, bw + bid, &ukeys, &m)) {
+      unsorted = true;   // de-duplicated in hashed buckets (one pass in shared memory)
+      tr.mark("bucket_unique");
     } else {
       if (!alt.p) alt.alloc(E, ctx);
       cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
@@ -754,6 +901,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       }, radix_kernels(E, bw + bid));
       in_keys = db.Current() == keys.p;
     }
+    if (!unsorted) {
     tr.mark("sort1");
     DevBuf<uint64_t>& sorted = in_keys ? keys : alt;
     DevBuf<uint64_t>& other = in_keys ? alt : keys;
@@ -773,6 +921,9 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     m = cnt - (cnt && last == kSentinel ? 1 : 0);
     ukeys = std::move(other);
     sorted.reset();
+    }
+    keys.reset();
+    alt.reset();
   }
   if (m >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
   g->m = m;
@@ -785,7 +936,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   g->okeys.alloc(m, ctx);
   if (n) {
     BBTC_CUDA(cudaMemsetAsync(deg.p, 0, (size_t)n * 4, st));
-    if (m && use_hash) {
+    if (m && unsorted) {
       k_degree_any<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
       BBTC_LAUNCHED(ctx);
     } else if (m) {

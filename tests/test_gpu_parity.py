@@ -525,3 +525,29 @@ def test_cut_refinement_and_study_tools(ctx):
         assert len(tt) == plan.n_tasks and np.all(tt >= 0) and tt.max() > 0
     cuts, mm = bb.refine_cuts(ctx, g, 3, cuts=[0, 10, 20, og.n], max_evals=60)
     assert mm <= int(bb.Plan(ctx, g, cuts=[0, 10, 20, og.n]).block_nnz().max())
+
+
+@pytest.mark.parametrize("heavy_dup", [False, True])
+def test_bucket_dedup(ctx, heavy_dup):
+    """a1 de-duplication in hashed buckets (device input, >= 2^22 raw pairs): the same
+    graph as the oracle's; one edge repeated 20,000 times overflows its bucket and the
+    sort path takes over — same result."""
+    import torch
+    import paper_2009_12457_b200 as bb
+    s, d = inputs.rmat(18, 20, 7)                       # 5.2 M raw pairs, K = 36 bits
+    if heavy_dup:
+        s = np.concatenate([s, np.full(20000, 5, np.uint32)])
+        d = np.concatenate([d, np.full(20000, 77, np.uint32)])
+    og = oracle.OracleGraph(s, d, 1 << 18)
+    ts = torch.from_numpy(s.view(np.int32)).cuda()
+    td = torch.from_numpy(d.view(np.int32)).cuda()
+    g = bb.Graph.from_edges(ctx, ts, td, 1 << 18)
+    assert g.size() == (og.n, og.m)
+    assert np.array_equal(g.rank(), og.rank())
+    row, col = g.csr()
+    orow, ocol = og.csr()
+    assert np.array_equal(row, orow) and np.array_equal(col, ocol)
+    plan = bb.Plan(ctx, g, 6)
+    tot, pt = plan.count()
+    otot, opt, _, _ = og.count(cuts=plan.cuts())
+    assert tot == otot and np.array_equal(pt, opt)
