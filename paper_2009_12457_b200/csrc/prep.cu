@@ -473,6 +473,48 @@ __global__ void k_low_bits(const K* __restrict__ keys, uint64_t m, int cb, uint3
     out[e] = (uint32_t)(keys[e] & mask);
 }
 
+// ---- a4 transpose by counting sort ---------------------------------------------------
+// Every block's column-major copy (ccu, ccv) from its row-major one: count each
+// (block, column), one exclusive scan over all blocks' columns in block order (which is
+// the arena order, so the scan yields global CSC positions), then scatter.  Two passes
+// and two atomics per edge instead of a 3-pass radix sort; the order of the rows inside
+// a column is arbitrary (nothing needs it: the kernel hashes lists, bit rows are sets).
+// Shared memory: the blocks' first edges (u64) and column bases (u64).
+__global__ void k_tr_count(const uint32_t* __restrict__ cols, uint64_t m, const BlockDesc* __restrict__ blocks,
+                           uint32_t nb, const uint64_t* __restrict__ cbase, uint32_t* __restrict__ cnt) {
+  extern __shared__ uint64_t s_tr[];
+  uint64_t* s_e0 = s_tr;
+  uint64_t* s_cb = s_tr + nb;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    s_e0[b] = blocks[b].e0;
+    s_cb[b] = cbase[b];
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = block_of_edge(s_e0, nb, e);
+    atomicAdd(&cnt[s_cb[b] + cols[e]], 1u);
+  }
+}
+__global__ void k_tr_scatter(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rows, uint64_t m,
+                             const BlockDesc* __restrict__ blocks, uint32_t nb, const uint64_t* __restrict__ cbase,
+                             uint32_t* __restrict__ cursor, uint32_t* __restrict__ ccu, uint32_t* __restrict__ ccv) {
+  extern __shared__ uint64_t s_tr[];
+  uint64_t* s_e0 = s_tr;
+  uint64_t* s_cb = s_tr + nb;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    s_e0[b] = blocks[b].e0;
+    s_cb[b] = cbase[b];
+  }
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = block_of_edge(s_e0, nb, e);
+    const uint32_t c = cols[e];
+    const uint32_t at = atomicAdd(&cursor[s_cb[b] + c], 1u);
+    ccu[at] = rows[e];
+    ccv[at] = c;
+  }
+}
+
 // ---- a1 bucket sort: canonical keys de-duplicated in hashed buckets -----------------
 // The K-bit keys (lo << bw | hi) are mixed by an odd multiplier mod 2^K (a bijection),
 // split into 2^BB buckets by the top BB mixed bits, and each bucket (<= kBktCap keys,
@@ -1176,7 +1218,36 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       BBTC_CUDA(cudaFuncSetAttribute(k_transpose_keys<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)key_smem));
     }
-    if (m && !batched) {
+    // Counting-sort transpose (default; BBTC_TRANSPOSE_SORT=1 keeps the radix sort).
+    uint64_t ncols_all = 0;
+    std::vector<uint64_t> colbase(nb);
+    for (uint32_t b = 0; b < nb; ++b) {
+      colbase[b] = ncols_all;
+      ncols_all += plan->blocks[b].nc;
+    }
+    const bool counting = !getenv("BBTC_TRANSPOSE_SORT") && (size_t)nb * 16 <= 200 * 1024 && ncols_all < (1ull << 32);
+    if (m && counting) {
+      DevBuf<uint32_t> cnt;
+      DevBuf<uint64_t> dcb;
+      cnt.alloc(ncols_all + 1, ctx);
+      dcb.alloc(nb, ctx);
+      BBTC_CUDA(cudaMemcpyAsync(dcb.p, colbase.data(), nb * 8, cudaMemcpyHostToDevice, st));
+      BBTC_CUDA(cudaMemsetAsync(cnt.p, 0, (ncols_all + 1) * 4, st));
+      const size_t sm = (size_t)nb * 16;
+      if (sm > 48 * 1024) {
+        BBTC_CUDA(cudaFuncSetAttribute(k_tr_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        BBTC_CUDA(cudaFuncSetAttribute(k_tr_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      }
+      k_tr_count<<<grid_for(ctx, m), kThreads, sm, st>>>(plan->cols.p, m, plan->d_blocks.p, nb, dcb.p, cnt.p);
+      BBTC_LAUNCHED(ctx);
+      cub_call(ctx, [&](void* t, size_t& bb) {
+        return cub::DeviceScan::ExclusiveSum(t, bb, cnt.p, cnt.p, ncols_all + 1, st);
+      });
+      k_tr_scatter<<<grid_for(ctx, m), kThreads, sm, st>>>(plan->cols.p, plan->rows.p, m, plan->d_blocks.p, nb,
+                                                            dcb.p, cnt.p, plan->ccu.p, plan->ccv.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaStreamSynchronize(st));   // (colbase is the host source of an async copy)
+    } else if (m && !batched) {
       // Few blocks: sort each block in place by its local column (no key pass).
       for (uint32_t b = 0; b < nb; ++b) {
         const BlockDesc& B = plan->blocks[b];

@@ -448,7 +448,8 @@ def test_auto_p_from_budget(ctx):
 
 def test_packed_transpose_keys(gpu):
     """Packed transpose keys (per-block column ranges minus the isolated prefix of each
-    part): forced on, with isolated vertices spanning several parts of user cuts."""
+    part): the radix-sort transpose forced on (the default is the counting sort), with
+    isolated vertices spanning several parts of user cuts."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -465,7 +466,8 @@ def test_packed_transpose_keys(gpu):
             "    plan = bb.Plan(ctx, g, p or 1, None if cuts is None else np.array(cuts, np.uint32))\n"
             "    t, pt = plan.count(); out.append([t, pt.tolist(), plan.cuts().tolist()])\n"
             "print(json.dumps(out))\n") % (root, n, cuts_user.tolist())
-    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1"},
+    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1",
+                                                            "BBTC_TRANSPOSE_SORT": "1"},
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     for tot, pt, cuts in json.loads(res.stdout.strip().splitlines()[-1]):
