@@ -473,6 +473,46 @@ __global__ void k_low_bits(const K* __restrict__ keys, uint64_t m, int cb, uint3
     out[e] = (uint32_t)(keys[e] & mask);
 }
 
+// ---- a4 CSR by counting sort -------------------------------------------------------
+// The row-offset arena is the counter array: every oriented edge (ru, rw) of block
+// (i, j) counts into rowptr[ro[b] + ru - cuts[i]]; one exclusive scan over the whole
+// arena gives every row's first edge in the arena (blocks in order, rows ascending,
+// each block's trailing entry = its end); a scatter places the edges (the order of
+// the columns inside a row is arbitrary, as before).  Replaces the (j, ru) radix sort.
+__global__ void k_csr_count(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
+                            uint32_t p, const uint64_t* __restrict__ ro, uint32_t* __restrict__ cnt) {
+  extern __shared__ uint32_t s_cuts[];
+  for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = okeys[e];
+    const uint32_t ru = (uint32_t)(k >> 32), rw = (uint32_t)k;
+    const uint32_t i = part_of(s_cuts, p, ru), j = part_of(s_cuts, p, rw);
+    atomicAdd(&cnt[ro[j * (j + 1) / 2 + i] + (ru - s_cuts[i])], 1u);
+  }
+}
+__global__ void k_csr_scatter(const uint64_t* __restrict__ okeys, uint64_t m, const uint32_t* __restrict__ gcuts,
+                              uint32_t p, const uint64_t* __restrict__ ro, uint32_t* __restrict__ cursor,
+                              uint32_t* __restrict__ cols, uint32_t* __restrict__ rows) {
+  extern __shared__ uint32_t s_cuts[];
+  for (uint32_t x = threadIdx.x; x <= p; x += blockDim.x) s_cuts[x] = gcuts[x];
+  __syncthreads();
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = okeys[e];
+    const uint32_t ru = (uint32_t)(k >> 32), rw = (uint32_t)k;
+    const uint32_t i = part_of(s_cuts, p, ru), j = part_of(s_cuts, p, rw);
+    const uint32_t lr = ru - s_cuts[i];
+    const uint32_t at = atomicAdd(&cursor[ro[j * (j + 1) / 2 + i] + lr], 1u);
+    cols[at] = rw - s_cuts[j];
+    rows[at] = lr;
+  }
+}
+// starts[b] = the arena position of block b's first edge (its first row offset).
+__global__ void k_block_first(const uint32_t* __restrict__ rowptr, const uint64_t* __restrict__ ro, uint32_t nb,
+                              uint64_t* __restrict__ starts) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) starts[b] = rowptr[ro[b]];
+}
+
 // ---- a4 transpose by counting sort ---------------------------------------------------
 // Every block's column-major copy (ccu, ccv) from its row-major one: count each
 // (block, column), one exclusive scan over all blocks' columns in block order (which is
@@ -1106,10 +1146,47 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   BBTC_CUDA(cudaMemcpyAsync(dcuts.p, plan->cuts.data(), (pe + 1) * 4, cudaMemcpyHostToDevice, st));
   // ---- a4: block-ordered keys
   DevBuf<uint64_t> ck, ck_alt;
-  ck.alloc(m, ctx);
   std::vector<uint64_t> starts(nb + 1, 0);
   const size_t cut_smem = (pe + 1) * 4;
-  if (m) {
+  // CSR by counting sort (default; BBTC_CSR_SORT=1 keeps the block-key radix sort)
+  std::vector<uint64_t> ro_h(nb + 1, 0);
+  for (uint32_t j = 0; j < pe; ++j)
+    for (uint32_t i = 0; i <= j; ++i) {
+      const uint32_t b = block_id(i, j);
+      ro_h[b + 1] = (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
+    }
+  for (uint32_t b = 0; b < nb; ++b) ro_h[b + 1] += ro_h[b];
+  const bool csr_count = !getenv("BBTC_CSR_SORT") && ro_h[nb] < (1ull << 32) && m;
+  if (csr_count) {
+    plan->rowptr.alloc(ro_h[nb], ctx);
+    plan->cols.alloc(m, ctx);
+    plan->rows.alloc(m, ctx);
+    DevBuf<uint64_t> dro, dstarts;
+    dro.alloc(nb + 1, ctx);
+    dstarts.alloc(nb, ctx);
+    BBTC_CUDA(cudaMemcpyAsync(dro.p, ro_h.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, st));
+    BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0, ro_h[nb] * 4, st));
+    k_csr_count<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(g->okeys.p, m, dcuts.p, pe, dro.p, plan->rowptr.p);
+    BBTC_LAUNCHED(ctx);
+    cub_call(ctx, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, plan->rowptr.p, plan->rowptr.p, ro_h[nb], st);
+    });
+    k_block_first<<<(nb + 255) / 256, 256, 0, st>>>(plan->rowptr.p, dro.p, nb, dstarts.p);
+    BBTC_LAUNCHED(ctx);
+    BBTC_CUDA(cudaMemcpyAsync(starts.data(), dstarts.p, nb * 8, cudaMemcpyDeviceToHost, st));
+    {
+      DevBuf<uint32_t> cursor;
+      cursor.alloc(ro_h[nb], ctx);
+      BBTC_CUDA(cudaMemcpyAsync(cursor.p, plan->rowptr.p, ro_h[nb] * 4, cudaMemcpyDeviceToDevice, st));
+      k_csr_scatter<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(g->okeys.p, m, dcuts.p, pe, dro.p, cursor.p,
+                                                                  plan->cols.p, plan->rows.p);
+      BBTC_LAUNCHED(ctx);
+      BBTC_CUDA(cudaStreamSynchronize(st));
+    }
+    starts[nb] = m;
+    tr.mark("csr_count");
+  } else if (m) {
+    ck.alloc(m, ctx);
     k_block_keys<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(g->okeys.p, m, dcuts.p, pe, bn, ck.p);
     BBTC_LAUNCHED(ctx);
     tr.mark("block_keys");
@@ -1149,11 +1226,12 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       m_max = std::max(m_max, B.nnz);
       bytes += 8 * B.nnz + 4 * ((uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1);
     }
+  plan->d_blocks.alloc(nb, ctx);
+  BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
+  if (!csr_count) {
   plan->cols.alloc(m, ctx);
   plan->rows.alloc(m, ctx);
   plan->rowptr.alloc(ro, ctx);
-  plan->d_blocks.alloc(nb, ctx);
-  BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
   BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0xFF, ro * 4, st));
   if (m) {
     k_split<<<grid_for(ctx, m), kThreads, cut_smem, st>>>(ck.p, m, dcuts.p, pe, bn, plan->d_blocks.p, plan->cols.p,
@@ -1170,6 +1248,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     cub_call(ctx, [&](void* t, size_t& b) {
       return cub::DeviceScan::InclusiveScan(t, b, rin, rin, MinOp{}, (uint64_t)ro, st);
     });
+  }
   }
   {
     uint32_t maxv = 0;
