@@ -448,8 +448,8 @@ def test_auto_p_from_budget(ctx):
 
 def test_packed_transpose_keys(gpu):
     """Packed transpose keys (per-block column ranges minus the isolated prefix of each
-    part): the radix-sort transpose forced on (the default is the counting sort), with
-    isolated vertices spanning several parts of user cuts."""
+    part): the radix-sort CSR and transpose forced on (the defaults are counting sorts),
+    with isolated vertices spanning several parts of user cuts."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -467,7 +467,7 @@ def test_packed_transpose_keys(gpu):
             "    t, pt = plan.count(); out.append([t, pt.tolist(), plan.cuts().tolist()])\n"
             "print(json.dumps(out))\n") % (root, n, cuts_user.tolist())
     res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1",
-                                                            "BBTC_TRANSPOSE_SORT": "1"},
+                                                            "BBTC_TRANSPOSE_SORT": "1", "BBTC_CSR_SORT": "1"},
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     for tot, pt, cuts in json.loads(res.stdout.strip().splitlines()[-1]):
