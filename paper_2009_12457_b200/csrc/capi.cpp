@@ -127,6 +127,23 @@ void ctx_free(bbtc_ctx* ctx, void* p, size_t bytes) {
   ctx->cached_bytes += sz;
 }
 
+// Estimated cost of one edge (u,v) of G_ij in task (i,j,k), in list words (sizes work
+// items; the multi-GPU scheduler's LPT weight).  "probe" (default, round 2): the probe
+// list d(G_ik,u) is walked per edge while the staged list N(G_jk,v) is hashed once per
+// column run, i.e. per edge in proportion to the non-empty columns of G_ij:
+// 4 + δ(G_ik) + min(1, |V_j| / nnz_ij)·δ(G_jk) — the estimator that ranks measured task
+// work best (ρ 0.87-0.93 on rmat24 / orkut / friendster, §10).  "paper+" (BBTC_ITEM_COST=
+// merge, round 1): 8 + δ(G_ik) + δ(G_jk), the merge cost of Alg. 1.
+static inline double edge_cost(double d_ik, double d_jk, double nnz_ij, double vj) {
+  static const bool merge = [] {
+    const char* e = getenv("BBTC_ITEM_COST");
+    return e && std::string(e) == "merge";
+  }();
+  if (merge) return 8.0 + d_ik + d_jk;
+  const double run = nnz_ij > 0 ? std::min(1.0, vj / nnz_ij) : 1.0;
+  return 4.0 + d_ik + run * d_jk;
+}
+
 static inline uint64_t C2(uint64_t n) { return n < 2 ? 0 : n * (n - 1) / 2; }
 static inline uint64_t C3(uint64_t n) { return n < 3 ? 0 : n * (n - 1) * (n - 2) / 6; }
 
@@ -166,7 +183,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
       for (uint32_t i = 0; i <= j; ++i)
         if (mine(i, j, k))
           work_total += (double)plan->blocks[block_id(i, j)].nnz *
-                        (8.0 + delta(block_id(i, k)) + delta(block_id(j, k)));
+                        edge_cost(delta(block_id(i, k)), delta(block_id(j, k)), (double)plan->blocks[block_id(i, j)].nnz,
+                                  (double)(plan->cuts[j + 1] - plan->cuts[j]));
   // ~384 items per warp slot of a full B200 (148 SMs x 40 warps); BBTC_ITEMS_PER_SLOT
   // overrides.  The estimate is uniform over a task's edges while the real cost is not
   // (hub columns: long runs x long probe lists), so fine items balance the tail:
@@ -271,7 +289,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
         // A list edge costs its lists; a dense edge a fixed number of bit-row words.
         // Dense tasks take the smaller of both chunks: without resident blocks (streamed,
         // out of core) the list kernel runs them too.
-        double per_edge = 8.0 + delta(T.ik) + delta(T.jk);
+        double per_edge = edge_cost(delta(T.ik), delta(T.jk), (double)plan->blocks[T.ij].nnz,
+                                    (double)(plan->cuts[j + 1] - plan->cuts[j]));
         if (plan->tasks.size() >= plan->dense_task_lo) per_edge = std::max(per_edge, 2.0 + plan->dense_s[k] / 8.0);
         uint64_t chunk = (uint64_t)(item_work / per_edge);
         chunk = std::max<uint64_t>(64, std::min<uint64_t>(1u << 16, (chunk + 31) / 32 * 32));
@@ -353,7 +372,8 @@ void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32
   for (uint32_t i = 0; i < p; ++i)
     for (uint32_t j = i; j < p; ++j)
       for (uint32_t k = j; k < p; ++k) {
-        const double w = (double)bnnz[block_id(i, j)] * (8.0 + delta(i, k) + delta(j, k));
+        const double w = (double)bnnz[block_id(i, j)] *
+                         edge_cost(delta(i, k), delta(j, k), (double)bnnz[block_id(i, j)], (double)rows(j));
         ts.push_back({w, task_index(p, i, j, k), i, j, k});
         total += w;
       }

@@ -30,11 +30,17 @@ def _random_blocks(rng, p, n=10000):
 
 
 def _work(p, cuts, bnnz):
+    """The scheduler's documented per-edge cost (capi.cpp edge_cost):
+    4 + δ(G_ik) + min(1, |V_j| / nnz_ij)·δ(G_jk) per edge of G_ij."""
     rows = np.diff(cuts.astype(np.float64))
     bid = lambda i, j: j * (j + 1) // 2 + i  # noqa: E731
     d = lambda i, j: bnnz[bid(i, j)] / rows[i] if rows[i] else 0.0  # noqa: E731
-    return [float(bnnz[bid(i, j)]) * (8 + d(i, k) + d(j, k)) for i in range(p) for j in range(i, p)
-            for k in range(j, p)]
+
+    def cost(i, j, k):
+        nij = float(bnnz[bid(i, j)])
+        run = min(1.0, rows[j] / nij) if nij > 0 else 1.0
+        return nij * (4 + d(i, k) + run * d(j, k))
+    return [cost(i, j, k) for i in range(p) for j in range(i, p) for k in range(j, p)]
 
 
 @pytest.mark.parametrize("p,world,seed", [(1, 2, 0), (4, 2, 1), (8, 3, 2), (12, 8, 3), (16, 8, 4), (30, 5, 5)])
