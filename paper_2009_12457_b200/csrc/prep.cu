@@ -728,7 +728,9 @@ __global__ void k_narrow(uint64_t* __restrict__ keys, uint64_t m, int bw) {
 
 }  // namespace
 
-// a1 bucket de-duplication of keys[0, E) (K live bits; sentinels skipped).  Returns
+// a1 bucket de-duplication of keys[0, E) (K live bits; sentinels skipped), BBTC_BUCKET=1:
+// measured slower than the onesweep sort + unique on B200 (rmat24 20.2 vs 17.5 ms, and
+// the unsorted keys cost the degree pass 6.4 vs 2.5 ms), kept as an option.  Returns
 // false (nothing done) when it does not apply: a bucket above kBktCap keys (heavy
 // duplication of one edge) or sizes outside its range — the caller sorts instead.
 static bool bucket_unique(bbtc_ctx* ctx, const uint64_t* keys, uint64_t E, int K, DevBuf<uint64_t>* ukeys,
@@ -972,7 +974,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       }
       in_keys = sel == 0;
       sort_tmp.reset();
-    } else if (!getenv("BBTC_NO_BUCKET") && bucket_unique(ctx, keys.p, E, bw + bid, &ukeys, &m)) {
+    } else if (getenv("BBTC_BUCKET") && bucket_unique(ctx, keys.p, E, bw + bid, &ukeys, &m)) {
       unsorted = true;   // de-duplicated in hashed buckets (one pass in shared memory)
       tr.mark("bucket_unique");
     } else {
@@ -1148,7 +1150,8 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
   DevBuf<uint64_t> ck, ck_alt;
   std::vector<uint64_t> starts(nb + 1, 0);
   const size_t cut_smem = (pe + 1) * 4;
-  // CSR by counting sort (default; BBTC_CSR_SORT=1 keeps the block-key radix sort)
+  // CSR by counting sort (BBTC_CSR_COUNT=1; measured slower than the block-key radix
+  // sort on B200: rmat24 34.7 vs ~13 ms, the random atomics into the row-offset arena)
   std::vector<uint64_t> ro_h(nb + 1, 0);
   for (uint32_t j = 0; j < pe; ++j)
     for (uint32_t i = 0; i <= j; ++i) {
@@ -1156,7 +1159,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       ro_h[b + 1] = (uint64_t)(plan->cuts[i + 1] - plan->cuts[i]) + 1;
     }
   for (uint32_t b = 0; b < nb; ++b) ro_h[b + 1] += ro_h[b];
-  const bool csr_count = !getenv("BBTC_CSR_SORT") && ro_h[nb] < (1ull << 32) && m;
+  const bool csr_count = getenv("BBTC_CSR_COUNT") && ro_h[nb] < (1ull << 32) && m;
   if (csr_count) {
     plan->rowptr.alloc(ro_h[nb], ctx);
     plan->cols.alloc(m, ctx);
@@ -1297,14 +1300,15 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       BBTC_CUDA(cudaFuncSetAttribute(k_transpose_keys<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)key_smem));
     }
-    // Counting-sort transpose (default; BBTC_TRANSPOSE_SORT=1 keeps the radix sort).
+    // Counting-sort transpose (BBTC_TRANSPOSE_COUNT=1; measured no faster than the
+    // packed-key radix sort on rmat24: 8.9 vs 8.4 ms).
     uint64_t ncols_all = 0;
     std::vector<uint64_t> colbase(nb);
     for (uint32_t b = 0; b < nb; ++b) {
       colbase[b] = ncols_all;
       ncols_all += plan->blocks[b].nc;
     }
-    const bool counting = !getenv("BBTC_TRANSPOSE_SORT") && (size_t)nb * 16 <= 200 * 1024 && ncols_all < (1ull << 32);
+    const bool counting = getenv("BBTC_TRANSPOSE_COUNT") && (size_t)nb * 16 <= 200 * 1024 && ncols_all < (1ull << 32);
     if (m && counting) {
       DevBuf<uint32_t> cnt;
       DevBuf<uint64_t> dcb;

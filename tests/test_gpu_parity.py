@@ -448,8 +448,7 @@ def test_auto_p_from_budget(ctx):
 
 def test_packed_transpose_keys(gpu):
     """Packed transpose keys (per-block column ranges minus the isolated prefix of each
-    part): the radix-sort CSR and transpose forced on (the defaults are counting sorts),
-    with isolated vertices spanning several parts of user cuts."""
+    part): forced on, with isolated vertices spanning several parts of user cuts."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -466,8 +465,7 @@ def test_packed_transpose_keys(gpu):
             "    plan = bb.Plan(ctx, g, p or 1, None if cuts is None else np.array(cuts, np.uint32))\n"
             "    t, pt = plan.count(); out.append([t, pt.tolist(), plan.cuts().tolist()])\n"
             "print(json.dumps(out))\n") % (root, n, cuts_user.tolist())
-    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1",
-                                                            "BBTC_TRANSPOSE_SORT": "1", "BBTC_CSR_SORT": "1"},
+    res = subprocess.run([sys.executable, "-c", code], env={**os.environ, "BBTC_PACKED_TRANSPOSE": "1"},
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     for tot, pt, cuts in json.loads(res.stdout.strip().splitlines()[-1]):
@@ -553,3 +551,26 @@ def test_bucket_dedup(ctx, heavy_dup):
     tot, pt = plan.count()
     otot, opt, _, _ = og.count(cuts=plan.cuts())
     assert tot == otot and np.array_equal(pt, opt)
+
+
+def test_counting_sort_options(gpu):
+    """The measured-and-dropped preprocessing options stay correct: bucket
+    de-duplication, CSR and transpose by counting sort (BBTC_BUCKET / BBTC_CSR_COUNT /
+    BBTC_TRANSPOSE_COUNT), on device input large enough for the buckets."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, numpy as np, torch; sys.path.insert(0, %r); import inputs, paper_2009_12457_b200 as bb\n"
+            "s, d = inputs.rmat(18, 20, 7); ctx = bb.Context(0)\n"
+            "g = bb.Graph.from_edges(ctx, torch.from_numpy(s.view(np.int32)).cuda(), torch.from_numpy(d.view(np.int32)).cuda(), 1 << 18)\n"
+            "row, col = g.csr(); plan = bb.Plan(ctx, g, 6); t, pt = plan.count()\n"
+            "print(json.dumps([t, pt.tolist(), plan.cuts().tolist(), g.rank().tolist()[:1000], int(row[-1])]))\n") % root
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "BBTC_BUCKET": "1", "BBTC_CSR_COUNT": "1", "BBTC_TRANSPOSE_COUNT": "1"})
+    assert res.returncode == 0, res.stderr[-2000:]
+    tot, pt, cuts, rank0, m = json.loads(res.stdout.strip().splitlines()[-1])
+    s, d = inputs.rmat(18, 20, 7)
+    og = oracle.OracleGraph(s, d, 1 << 18)
+    otot, opt, _, _ = og.count(cuts=np.asarray(cuts, np.uint32))
+    assert tot == otot and pt == [int(x) for x in opt] and m == og.m
+    assert rank0 == og.rank().tolist()[:1000]
