@@ -541,7 +541,11 @@ def test_bucket_dedup(ctx, heavy_dup):
     og = oracle.OracleGraph(s, d, 1 << 18)
     ts = torch.from_numpy(s.view(np.int32)).cuda()
     td = torch.from_numpy(d.view(np.int32)).cuda()
-    g = bb.Graph.from_edges(ctx, ts, td, 1 << 18)
+    os.environ["BBTC_BUCKET"] = "1"                   # (an option, off by default: DESIGN §7)
+    try:
+        g = bb.Graph.from_edges(ctx, ts, td, 1 << 18)
+    finally:
+        del os.environ["BBTC_BUCKET"]
     assert g.size() == (og.n, og.m)
     assert np.array_equal(g.rank(), og.rank())
     row, col = g.csr()
