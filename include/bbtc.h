@@ -333,6 +333,15 @@ BBTC_API bbtc_status bbtc_count_hybrid(bbtc_ctx* ctx, const bbtc_plan* plan, con
 BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan);
 /* Drops the device copies made by bbtc_stage / streaming counts. */
 BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan);
+/* §8(e) "each block H2D once, by its owner": copies blocks ids[0..n) of a host plan
+ * (bbtc_plan_to_host) to the device in their device form (synchronous).  The other
+ * blocks a rank's tasks read arrive from their owners over NVLink (bbtc_plan_block_ptrs
+ * + the caller's transfer); the caller then passes BBTC_STAGE_RESIDENT (with n = 0 or
+ * the last ids) to declare every block its tasks read present, and counts as resident.
+ * Errors: BBTC_ESTATE (not a host plan), BBTC_EINVAL (bad id). */
+#define BBTC_STAGE_RESIDENT 1u
+BBTC_API bbtc_status bbtc_stage_blocks(bbtc_ctx* ctx, bbtc_plan* plan, const uint32_t* ids, uint32_t n,
+                                       uint32_t flags);
 
 /* ------------------------------------------- multi-GPU sharded build (§8(e))
  * One process per GPU, rank r of `world`, each starting from its own share of the

@@ -263,6 +263,11 @@ class Plan:
     def stage(self):
         L.check(L.bbtc_stage(self.ctx.handle, self._h))
 
+    def stage_blocks(self, ids, resident: bool = False):
+        """bbtc_stage_blocks: copy these blocks of a host plan to the device (§8(e) owner copy)."""
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        L.check(L.bbtc_stage_blocks(self.ctx.handle, self._h, a.ctypes.data_as(L._u32p), len(a), 1 if resident else 0))
+
     def unstage(self):
         L.check(L.bbtc_unstage(self.ctx.handle, self._h))
 

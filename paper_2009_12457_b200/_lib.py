@@ -124,6 +124,7 @@ bbtc_task_times = _sig("bbtc_task_times", _st, _vp, _vp, ctypes.POINTER(ctypes.c
 bbtc_cuts_refine = _sig("bbtc_cuts_refine", _st, _vp, _vp, c_u32, _u32p, c_u32, _u32p, _u64p)
 bbtc_stage = _sig("bbtc_stage", _st, _vp, _vp)
 bbtc_unstage = _sig("bbtc_unstage", _st, _vp, _vp)
+bbtc_stage_blocks = _sig("bbtc_stage_blocks", _st, _vp, _vp, _u32p, c_u32, c_u32)
 bbtc_shard_canon = _sig("bbtc_shard_canon", _st, _vp, _vp, _vp, c_u64, ctypes.c_int, c_u32, c_u32, _vp, _u64p,
                         _u32p)
 bbtc_shard_graph = _sig("bbtc_shard_graph", _st, _vp, _vp, c_u64, c_u32, _vp, _pp)

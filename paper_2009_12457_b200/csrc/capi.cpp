@@ -875,6 +875,36 @@ BBTC_API bbtc_status bbtc_stage(bbtc_ctx* ctx, bbtc_plan* plan) {
   });
 }
 
+BBTC_API bbtc_status bbtc_stage_blocks(bbtc_ctx* ctx, bbtc_plan* plan, const uint32_t* ids, uint32_t n,
+                                       uint32_t flags) {
+  return guard([&] {
+    if (!ctx || !plan || (n && !ids)) raise(BBTC_EINVAL, "NULL argument");
+    if (!plan->host_blocks) raise(BBTC_ESTATE, "the plan's blocks are not in host memory (bbtc_plan_to_host)");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    if (plan->resident && n) return;   // everything is on the device already
+    ensure_device_arenas(ctx, plan);
+    auto arenas = plan->edge_arenas();
+    for (uint32_t x = 0; x < n; ++x) {
+      const uint32_t b = ids[x];
+      if (b >= plan->blocks.size()) raise(BBTC_EINVAL, "block id >= p(p+1)/2");
+      const BlockDesc& B = plan->blocks[b];
+      cudaStream_t cs = ctx->copy_streams[x % ctx->copy_streams.size()];
+      for (auto& A : arenas)   // the block's device form as it is (incl. ccv: no expansion step)
+        if (B.nnz)
+          BBTC_CUDA(cudaMemcpyAsync(A.dev->p + B.e0, *A.host + B.e0, B.nnz * 4, cudaMemcpyHostToDevice, cs));
+      const uint64_t rlen = (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+      BBTC_CUDA(cudaMemcpyAsync(plan->rowptr.p + B.ro, plan->h_rowptr + B.ro, rlen * 4, cudaMemcpyHostToDevice, cs));
+    }
+    for (auto cs : ctx->copy_streams) BBTC_CUDA(cudaStreamSynchronize(cs));
+    if (flags & BBTC_STAGE_RESIDENT) {
+      plan->d_colptr.reset();
+      plan->dense.reset();
+      plan->dense_ready = false;
+      plan->resident = true;
+    }
+  });
+}
+
 BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
   return guard([&] {
     if (!ctx || !plan) raise(BBTC_EINVAL, "NULL argument");
@@ -1393,7 +1423,7 @@ BBTC_API bbtc_status bbtc_plan_block_ptrs(const bbtc_plan* plan, uint32_t b, bbt
   return guard([&] {
     if (!plan || !out) raise(BBTC_EINVAL, "NULL argument");
     if (b >= plan->blocks.size()) raise(BBTC_EINVAL, "block id >= p(p+1)/2");
-    if (!plan->resident) raise(BBTC_ESTATE, "blocks are not device-resident");
+    if (!plan->rowptr.p) raise(BBTC_ESTATE, "the plan has no device arenas (bbtc_stage / bbtc_stage_blocks)");
     bbtc_plan* pl = const_cast<bbtc_plan*>(plan);
     const BlockDesc& B = plan->blocks[b];
     auto arenas = pl->edge_arenas();

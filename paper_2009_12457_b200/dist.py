@@ -154,12 +154,18 @@ def task_blocks(p: int):
     return out
 
 
-def block_routes(p: int, task_rank, block_rank, block_nnz):
-    """[(block, owner, [receiving ranks])] for every non-empty block some other rank needs."""
+def block_readers(p: int, task_rank):
+    """{block: set of ranks whose tasks read it}."""
     need = {}
     for t, bl in enumerate(task_blocks(p)):
         for b in bl:
             need.setdefault(b, set()).add(int(task_rank[t]))
+    return need
+
+
+def block_routes(p: int, task_rank, block_rank, block_nnz):
+    """[(block, owner, [receiving ranks])] for every non-empty block some other rank needs."""
+    need = block_readers(p, task_rank)
     routes = []
     for b in sorted(need):
         if int(block_nnz[b]) == 0:
@@ -317,3 +323,33 @@ def build_sharded(ctx, src, dst, n_hint: int, p: int, cuts=None, group=None, fla
             "tasks_here": int((task_rank == rank).sum())}
     return g, plan, info
 
+
+
+def count_owner_h2d(ctx, plan, info, counts, group=None):
+    """§8(e) "copy each block H2D once, by its owner, and forward it over NVLink", for a
+    shard plan whose blocks are in pinned host memory (plan.to_host()): this rank copies
+    the blocks it owns that some task reads (bbtc_stage_blocks), receives the others it
+    needs from their owners (NCCL P2P), counts its tasks and joins the all-reduce.
+    Returns (h2d bytes of this rank, NVLink bytes received)."""
+    import torch
+    world, rank = _world_rank(group)
+    p = info["p"]
+    need = block_readers(p, info["task_rank"])
+    owned = [b for b, rs in sorted(need.items()) if int(info["block_rank"][b]) == rank and int(info["block_nnz"][b])]
+    cuts = info["cuts"]
+    h2d = 0
+    for b in owned:
+        j = int((np.sqrt(8 * b + 1) - 1) // 2)
+        while (j + 1) * (j + 2) // 2 <= b:
+            j += 1
+        i = b - j * (j + 1) // 2
+        h2d += 12 * int(info["block_nnz"][b]) + 4 * (int(cuts[i + 1] - cuts[i]) + 1)
+    plan.unstage()
+    plan.stage_blocks(owned)
+    routes = block_routes(p, info["task_rank"], info["block_rank"], info["block_nnz"])
+    _, got = forward_blocks(plan, routes, torch.device("cuda", ctx.device), group)
+    plan.stage_blocks([], resident=True)
+    plan.count_async(counts, rank, world)
+    _after_ctx_stream(ctx, counts)
+    reduce_counts(counts, group)
+    return h2d, got

@@ -117,8 +117,16 @@ def _shard_worker(rank, world, port, q, spec, p, host_input, backend):
     mine = counts.cpu().numpy().view(np.uint64).copy()
     count_distributed(plan, counts)
     torch.cuda.synchronize()
-    q.put((rank, counts.cpu().numpy().view(np.uint64).tolist(), mine.tolist(), info["cuts"].tolist(),
-           info["h2d_bytes"], b - a, info["tasks_here"], info["nvlink_bytes_recv"], info["m"], info["n"]))
+    full = counts.cpu().numpy().view(np.uint64).tolist()
+    # incl. H2D: blocks in pinned host memory, each copied once by its owner, forwarded
+    from paper_2009_12457_b200.dist import count_owner_h2d
+    plan.to_host()
+    h2d_blocks, _ = count_owner_h2d(ctx, plan, info, counts)
+    torch.cuda.synchronize()
+    full_h = counts.cpu().numpy().view(np.uint64).tolist()
+    q.put((rank, full, mine.tolist(), info["cuts"].tolist(),
+           info["h2d_bytes"], b - a, info["tasks_here"], info["nvlink_bytes_recv"], info["m"], info["n"],
+           full_h, h2d_blocks, plan.info()["block_bytes"]))
     dist.destroy_process_group()
 
 
@@ -149,14 +157,19 @@ def test_sharded_build_matches_oracle(gpu, world, host_input):
     assert np.array_equal(cuts, og.default_cuts(6))                 # global default rule
     otot, opt, _, _ = og.count(cuts=cuts)
     partial = np.zeros(len(opt), np.uint64)
-    for rank, full, mine, c, h2d, share, ntasks, got, m, n in res:
+    h2d_total = 0
+    for rank, full, mine, c, h2d, share, ntasks, got, m, n, full_h, h2d_blocks, block_bytes in res:
         assert full[-1] == otot and full[:-1] == [int(x) for x in opt]
+        assert full_h == full                                          # owner-copy + NVLink path
+        h2d_total += h2d_blocks
+        assert h2d_blocks < block_bytes                                # no rank copies every block
         assert c == res[0][3] and (m, n) == (og.m, og.n)
         assert h2d == (8 * share if host_input else 0)               # per-rank H2D = its share
         partial += np.asarray(mine[:-1], np.uint64)
         assert 0 < ntasks < len(opt)
     assert np.array_equal(partial, opt)                                # ranks' tasks are disjoint
     assert sum(r[6] for r in res) == len(opt)
+    assert h2d_total <= res[0][12]                                     # every block crosses PCIe at most once
 
 
 def test_sharded_build_user_cuts_and_karate(gpu):
@@ -167,6 +180,7 @@ def test_sharded_build_user_cuts_and_karate(gpu):
     G = json.load(open(os.path.join(ROOT, "tests", "golden", "karate.json")))
     assert res[0][3] == G["default_cuts"]["2"]
     assert res[0][1][:-1] == G["per_task"][0]["counts"] and res[0][1][-1] == 45
+    assert res[0][10] == res[0][1]
 
 
 def test_nccl_single_rank_path(gpu):
