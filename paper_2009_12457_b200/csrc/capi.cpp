@@ -851,6 +851,7 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     }
     BBTC_CUDA(cudaStreamSynchronize(st));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
+    if (plan->colmajor) plan->rows.reset();   // (kept only for the dense row walk of resident plans)
     plan->rowptr.reset();
     plan->dense.reset();
     plan->dense_ready = false;

@@ -820,7 +820,9 @@ void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uin
   const int per = std::max(1, std::min(per_sm, kCtasPerSm));
   const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
   k_count_dense<<<(unsigned)grid, kWarps * 32, 0, st>>>(
-      plan->colmajor ? plan->ccu.p : plan->rows.p, plan->colmajor ? plan->ccv.p : plan->cols.p, plan->dense.p,
+      // row walk when the plan kept its row ids (row-major plans; BBTC_DENSE_WALK=row)
+      plan->colmajor && !plan->rows.p ? plan->ccu.p : plan->rows.p,
+      plan->colmajor && !plan->rows.p ? plan->ccv.p : plan->cols.p, plan->dense.p,
       plan->d_dense_off.p, plan->d_blocks.p, plan->d_tasks.p, plan->d_item_start.p, (uint32_t)plan->tasks.size(),
       item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts, (uint32_t)plan->info.n_tasks,
       (unsigned long long*)ctx->task_cycles);

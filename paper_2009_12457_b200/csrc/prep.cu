@@ -1384,7 +1384,10 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       k_low_bits<uint64_t><<<grid_for(ctx, m), kThreads, 0, st>>>(sorted.p, m, cb, plan->ccv.p);
       BBTC_LAUNCHED(ctx);
     }
-    plan->rows.reset();   // the row-major COO is only needed to build the transpose
+    // The row-major COO is only needed to build the transpose, unless the bit-row kernel
+    // walks dense tasks by row (BBTC_DENSE_WALK=row: rows of G_jk gathered instead of G_ik).
+    if (!(getenv("BBTC_DENSE_WALK") && std::string(getenv("BBTC_DENSE_WALK")) == "row" && plan->dense_bits))
+      plan->rows.reset();
     bytes += 4 * m;       // cols + ccu + ccv instead of cols + rows
     tr.mark("transpose");
   }
