@@ -200,9 +200,9 @@ CONFIGS = {
     "rmat16": Config("rmat16", "rmat", p=4, scale=16, desc="R-MAT scale 16 ef 16, 4x4 blocks"),
     "orkut": Config("orkut", "chunglu", p=8, n=3_072_441, m=117_185_083, gamma=2.3314, dmax=33_313,
                     desc="com-Orkut-shaped Chung-Lu, 8x8 blocks"),
-    # p = 12: the measured best step with bit rows up to 8192 bits (profiles/r01c/ab_dense_bits16k.jsonl;
-    # p = 12 / 14 / 16: 95.3 / 96.8 / 99.3 ms); SURVEY §8(d) proposed 16, the paper used 28.
-    "rmat24": Config("rmat24", "rmat", p=12, scale=24, desc="R-MAT scale 24 ef 16, 12x12 blocks"),
+    # p = 10: the measured best step in round 2 (profiles/r02/ab1: p = 8 / 10 / 12: 92.7 / 92.2 /
+    # 95.7 ms; round 1's sweep picked 12 of 12 / 14 / 16); SURVEY §8(d) proposed 16, the paper 28.
+    "rmat24": Config("rmat24", "rmat", p=10, scale=24, desc="R-MAT scale 24 ef 16, 10x10 blocks"),
     "friendster": Config("friendster", "chunglu", p=4, n=65_608_366, m=1_806_067_135, gamma=2.0,
                          dmax=5_214, desc="Friendster-shaped Chung-Lu, 4x4 blocks"),
 }
