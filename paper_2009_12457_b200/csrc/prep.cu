@@ -1386,7 +1386,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     }
     // The row-major COO is only needed to build the transpose, unless the bit-row kernel
     // walks dense tasks by row (BBTC_DENSE_WALK=row: rows of G_jk gathered instead of G_ik).
-    if (!(getenv("BBTC_DENSE_WALK") && std::string(getenv("BBTC_DENSE_WALK")) == "row" && plan->dense_bits))
+    if (!(getenv("BBTC_DENSE_WALK") && std::string(getenv("BBTC_DENSE_WALK")) == "row" && !(flags & BBTC_PLAN_SPARSE)))
       plan->rows.reset();
     bytes += 4 * m;       // cols + ccu + ccv instead of cols + rows
     tr.mark("transpose");
