@@ -1794,6 +1794,7 @@ void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* oke
   plan->shard_rank = rank;
   plan->shard_world = world;
   plan_build(ctx, &tg, p, cuts, flags & ~BBTC_PLAN_STATS, plan);
+  if (plan->colmajor) plan->rows.reset();   // (not moved to the global layout nor forwarded: dense tasks walk by column)
   tr.mark("local_build");
   // Re-lay the arenas out at the global block offsets.
   const uint32_t nb = p * (p + 1) / 2;
