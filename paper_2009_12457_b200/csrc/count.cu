@@ -53,6 +53,12 @@ constexpr bool kRunPipe = BBTC_RUN_PIPE;   // pipelined column runs (hash-only v
 #ifndef BBTC_RUN_PIPE_BM
 #define BBTC_RUN_PIPE_BM 0
 #endif
+#ifndef BBTC_LANEWALK
+#define BBTC_LANEWALK 0   // A/B: lanes walk their own < 32-word probe remainders when lengths are even
+#endif
+#ifndef BBTC_LANEWALK_K
+#define BBTC_LANEWALK_K 2  // lane walk when 32 * max remainder <= K * sum of remainders + 64
+#endif
 constexpr int kCarveoutPct = 0;      // shared-memory carveout in percent (0 = driver default)
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
@@ -159,6 +165,27 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
     for (; off < nfull; off += 32) hits += test(B[off], sl);
   }
   const uint32_t rem = bl & 31u;
+#if BBTC_LANEWALK
+  // Remainders of similar length: every lane walks its own (4 loads in flight) instead
+  // of the flattened walk, whose per-window owner search costs ~10 instructions.
+  const uint32_t rmax = __reduce_max_sync(kFull, rem);
+  const uint32_t rsum = __reduce_add_sync(kFull, rem);
+  if (rmax * 32 <= BBTC_LANEWALK_K * rsum + 64) {
+    const uint32_t* B = cols + bx + (bl & ~31u);
+    uint32_t x = 0;
+    for (; x + 4 <= rmax; x += 4) {
+      const uint32_t w0 = x < rem ? B[x] : 0u, w1 = x + 1 < rem ? B[x + 1] : 0u;
+      const uint32_t w2 = x + 2 < rem ? B[x + 2] : 0u, w3 = x + 3 < rem ? B[x + 3] : 0u;
+      if (x < rem) hits += test(w0, slot);
+      if (x + 1 < rem) hits += test(w1, slot);
+      if (x + 2 < rem) hits += test(w2, slot);
+      if (x + 3 < rem) hits += test(w3, slot);
+    }
+    for (; x < rmax; ++x)
+      if (x < rem) hits += test(B[x], slot);
+    return hits;
+  }
+#endif
   const uint32_t rinc = warp_incl_scan(rem, lane);
   const uint32_t total_r = __shfl_sync(kFull, rinc, 31);
   const uint32_t rstart = rinc - rem;
