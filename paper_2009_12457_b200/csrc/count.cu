@@ -563,7 +563,10 @@ __global__ void k_dense_rows(const uint32_t* __restrict__ it_u, const uint32_t* 
 // The edges [e_begin, e_end) of G_ij of one dense item, bit rows of stride S words:
 // 32 edges at a time; a round takes 32/LPR edges, LPR lanes per edge each loading Q
 // uint4 of both rows (kUnroll rounds of loads in flight).  Returns this lane's hits.
-template <int S>
+// kKeepU (row walk: consecutive edges share u): a lane keeps the row_ik(u) words it
+// last loaded and reloads them only when its edge's u changes, so only row_jk(v) is
+// read per edge (half the L1/L2 traffic of the bit-row kernel on long rows).
+template <int S, bool kKeepU>
 __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
                                                 const uint32_t* __restrict__ Dik, const uint32_t* __restrict__ Djk,
                                                 uint64_t e_begin, uint64_t e_end, int lane) {
@@ -577,6 +580,10 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
   const uint4* Di = reinterpret_cast<const uint4*>(Dik) + q;
   const uint4* Dj = reinterpret_cast<const uint4*>(Djk) + q;
   uint32_t acc = 0;
+  uint32_t ku = 0xFFFFFFFFu;   // kKeepU: the u whose row words this lane holds in ka
+  uint4 ka[Q];
+#pragma unroll
+  for (int x = 0; x < Q; ++x) ka[x] = make_uint4(0, 0, 0, 0);
   for (uint64_t base = e_begin; base < e_end; base += 32) {
     const uint64_t e = base + lane;
     const bool valid = e < e_end;
@@ -590,15 +597,21 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
       for (int r = 0; r < kUnroll; ++r) {
         const int idx = (r0 + r) * EPR + sub;
         const uint32_t uu = __shfl_sync(kFull, u, idx & 31), vv = __shfl_sync(kFull, v, idx & 31);
+        const bool fresh = !kKeepU || uu != ku;
 #pragma unroll
         for (int x = 0; x < Q; ++x) {
           if (idx < n) {
-            a[r][x] = Di[(uint64_t)uu * kV + x * LPR];
+            a[r][x] = fresh ? Di[(uint64_t)uu * kV + x * LPR] : ka[x];
             b[r][x] = Dj[(uint64_t)vv * kV + x * LPR];
           } else {
             a[r][x] = make_uint4(0, 0, 0, 0);
             b[r][x] = a[r][x];
           }
+        }
+        if (kKeepU && idx < n) {
+          ku = uu;
+#pragma unroll
+          for (int x = 0; x < Q; ++x) ka[x] = a[r][x];
         }
       }
 #pragma unroll
@@ -616,6 +629,7 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
 #ifndef BBTC_DENSE_MIN_CTAS
 #define BBTC_DENSE_MIN_CTAS 4
 #endif
+template <bool kKeepU>
 __global__ void __launch_bounds__(kWarps * 32, BBTC_DENSE_MIN_CTAS)
 k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
               const uint32_t* __restrict__ dense, const uint64_t* __restrict__ off,
@@ -645,13 +659,13 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
     const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
     uint32_t acc = 0;
     switch (T.pad) {
-      case 8: acc = dense_edges<8>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 16: acc = dense_edges<16>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 32: acc = dense_edges<32>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 64: acc = dense_edges<64>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 128: acc = dense_edges<128>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 256: acc = dense_edges<256>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      default: acc = dense_edges<512>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 8: acc = dense_edges<8, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 16: acc = dense_edges<16, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 32: acc = dense_edges<32, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 64: acc = dense_edges<64, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 128: acc = dense_edges<128, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 256: acc = dense_edges<256, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      default: acc = dense_edges<512, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
     }
     const uint32_t s = __reduce_add_sync(kFull, acc);
     if (lane == 0 && s) {
@@ -842,11 +856,14 @@ void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uin
   if (!ctx->cursor) BBTC_CUDA(cudaMalloc((void**)&ctx->cursor, 8 * kCursorSlots));
   unsigned long long* cursor = (unsigned long long*)ctx->cursor + (ctx->cursor_next++ % kCursorSlots);
   BBTC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+  // row walk (the plan kept its row ids): keep row_ik(u) across a row's edges
+  const bool row_walk = !plan->colmajor || plan->rows.p;
+  auto kern = row_walk && !getenv("BBTC_DENSE_NOKEEP") ? k_count_dense<true> : k_count_dense<false>;
   static int per_sm = 0;
-  if (!per_sm) BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_dense, kWarps * 32, 0));
+  if (!per_sm) BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_dense<true>, kWarps * 32, 0));
   const int per = std::max(1, std::min(per_sm, kCtasPerSm));
   const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
-  k_count_dense<<<(unsigned)grid, kWarps * 32, 0, st>>>(
+  kern<<<(unsigned)grid, kWarps * 32, 0, st>>>(
       // row walk when the plan kept its row ids (row-major plans; BBTC_DENSE_WALK=row)
       plan->colmajor && !plan->rows.p ? plan->ccu.p : plan->rows.p,
       plan->colmajor && !plan->rows.p ? plan->ccv.p : plan->cols.p, plan->dense.p,
