@@ -189,6 +189,7 @@ struct bbtc_plan {
   // so nothing the persistent count kernel waits for needs an SM).
   uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
   std::vector<uint64_t> rp_zero;      // per block: leading zero entries of its row offsets
+  std::vector<int> band_shift;        // per block: walk by (row >> shift, column) bands, -1 = plain columns
   std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;

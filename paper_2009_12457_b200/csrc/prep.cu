@@ -513,6 +513,20 @@ __global__ void k_block_first(const uint32_t* __restrict__ rowptr, const uint64_
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) starts[b] = rowptr[ro[b]];
 }
 
+// ---- a4 row bands (BBTC_BANDS, §7 "Row bands") --------------------------------------
+// key = (row >> shift) << cb | column: a block's column-major walk, split into bands of
+// 2^shift rows, so the probe lists a band gathers (rows of G_ik) stay L2-resident.
+__global__ void k_band_keys(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cols, uint64_t n,
+                            int shift, int cb, uint32_t* __restrict__ keys) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
+    keys[e] = ((rows[e] >> shift) << cb) | cols[e];
+}
+__global__ void k_band_cols(uint32_t* __restrict__ keys, uint64_t n, int cb) {
+  const uint32_t mask = (1u << cb) - 1;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
+    keys[e] &= mask;
+}
+
 // ---- a4 transpose by counting sort ---------------------------------------------------
 // Every block's column-major copy (ccu, ccv) from its row-major one: count each
 // (block, column), one exclusive scan over all blocks' columns in block order (which is
@@ -1331,11 +1345,44 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       BBTC_LAUNCHED(ctx);
       BBTC_CUDA(cudaStreamSynchronize(st));   // (colbase is the host source of an async copy)
     } else if (m && !batched) {
-      // Few blocks: sort each block in place by its local column (no key pass).
+      // Few blocks: sort each block in place by its local column (no key pass).  With
+      // row bands (BBTC_BANDS=1) the key is (row band, column): a block whose probe blocks
+      // G_ik (k >= j) exceed BBTC_BAND_BYTES (default 32 MB) is walked band by band.
+      static const bool bands = getenv("BBTC_BANDS") != nullptr;
+      static const double band_bytes = getenv("BBTC_BAND_BYTES") ? atof(getenv("BBTC_BAND_BYTES")) : 32e6;
+      plan->band_shift.assign(nb, -1);
       for (uint32_t b = 0; b < nb; ++b) {
         const BlockDesc& B = plan->blocks[b];
         if (B.nnz == 0) continue;
         const int bits = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
+        const uint32_t rows_i = plan->cuts[B.i + 1] - plan->cuts[B.i];
+        int shift = -1;
+        if (bands && rows_i > 1) {
+          double probe = 0;   // the largest probe block this block's tasks gather from
+          for (uint32_t k = B.j; k < pe; ++k)
+            probe = std::max(probe, 4.0 * (double)plan->blocks[block_id(B.i, k)].nnz + 4.0 * rows_i);
+          if (probe > band_bytes) {
+            const double band_rows = (double)rows_i * band_bytes / probe;
+            shift = std::max(0, (int)std::floor(std::log2(std::max(1.0, band_rows))));
+            if (bitlen((rows_i - 1) >> shift) + bits > 32) shift = -1;   // key must fit 32 bits
+          }
+        }
+        if (shift >= 0) {
+          DevBuf<uint32_t> keys;
+          keys.alloc(B.nnz, ctx);
+          k_band_keys<<<grid_for(ctx, B.nnz), kThreads, 0, st>>>(plan->rows.p + B.e0, plan->cols.p + B.e0, B.nnz,
+                                                                  shift, bits, keys.p);
+          BBTC_LAUNCHED(ctx);
+          const int kbits = bits + bitlen((rows_i - 1) >> shift);
+          cub_call(ctx, [&](void* t, size_t& bb) {
+            return cub::DeviceRadixSort::SortPairs(t, bb, keys.p, plan->ccv.p + B.e0, plan->rows.p + B.e0,
+                                                   plan->ccu.p + B.e0, B.nnz, 0, kbits, st);
+          }, radix_kernels(B.nnz, kbits));
+          k_band_cols<<<grid_for(ctx, B.nnz), kThreads, 0, st>>>(plan->ccv.p + B.e0, B.nnz, bits);
+          BBTC_LAUNCHED(ctx);
+          plan->band_shift[b] = shift;
+          continue;
+        }
         cub_call(ctx, [&](void* t, size_t& bb) {
           return cub::DeviceRadixSort::SortPairs(t, bb, plan->cols.p + B.e0, plan->ccv.p + B.e0, plan->rows.p + B.e0,
                                                  plan->ccu.p + B.e0, B.nnz, 0, bits, st);
@@ -1430,7 +1477,8 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
     // (>= 4 edges per column on average: with sparser columns the kernel's 32-column
     // windows cover too few edges per batch — rmat24 (1,1): 2 edges/column, the
     // column-offset walk 2.7x slower than reading ccv, scripts/dbg_cp_tasks.py)
-    const bool cp = B.nnz >= 4 * ((uint64_t)w + 1);
+    const bool cp = B.nnz >= 4 * ((uint64_t)w + 1) &&
+                    (plan->band_shift.empty() || plan->band_shift[b] < 0);   // (a banded column is split)
     if (cp) {
       maxw = std::max(maxw, w + 1);
       co[b] = plan->co_off[b];

@@ -578,3 +578,14 @@ def test_counting_sort_options(gpu):
     otot, opt, _, _ = og.count(cuts=np.asarray(cuts, np.uint32))
     assert tot == otot and pt == [int(x) for x in opt] and m == og.m
     assert rank0 == og.rank().tolist()[:1000]
+
+
+def test_row_bands_option(gpu):
+    """Row bands (BBTC_BANDS): blocks walked by (row band, column) give the
+    oracle's per-task counts in every mode; a tiny band budget forces many bands."""
+    s, d = inputs.rmat(16, 16, 9)
+    og = oracle.OracleGraph(s, d, 1 << 16)
+    modes = ["resident", "ranks3", "streamed", "ooc50", "stage"]
+    res = child("rmat:16:16:9", 4, modes, env={"BBTC_BANDS": "1", "BBTC_BAND_BYTES": "65536"})
+    otot, opt, _, _ = og.count(cuts=np.asarray(res["cuts"], np.uint32))
+    assert_modes(res, modes, otot, opt)
