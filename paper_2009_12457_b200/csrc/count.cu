@@ -54,7 +54,10 @@ constexpr bool kRunPipe = BBTC_RUN_PIPE;   // pipelined column runs (hash-only v
 #define BBTC_RUN_PIPE_BM 0
 #endif
 #ifndef BBTC_LANEWALK
-#define BBTC_LANEWALK 0   // A/B: lanes walk their own < 32-word probe remainders when lengths are even
+// Lanes walk their own < 32-word probe remainders when the lengths are even enough
+// (instead of the flattened walk): rmat24 p=10 list kernel 33.1 -> 32.2 ms, orkut and
+// friendster unchanged (profiles/r02/ab5; K = 3 / always: no better, friendster worse).
+#define BBTC_LANEWALK 1
 #endif
 #ifndef BBTC_LANEWALK_K
 #define BBTC_LANEWALK_K 2  // lane walk when 32 * max remainder <= K * sum of remainders + 64
@@ -858,7 +861,9 @@ void count_launch_dense(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uin
   BBTC_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
   // row walk (the plan kept its row ids): keep row_ik(u) across a row's edges
   const bool row_walk = !plan->colmajor || plan->rows.p;
-  auto kern = row_walk && !getenv("BBTC_DENSE_NOKEEP") ? k_count_dense<true> : k_count_dense<false>;
+  // (keeping row_ik(u) in registers across a row's edges measured slower: rmat24 p=10
+  // 11.4 -> 12.9 ms — more registers, and the reloads hit L1 anyway; BBTC_DENSE_KEEP=1)
+  auto kern = row_walk && getenv("BBTC_DENSE_KEEP") ? k_count_dense<true> : k_count_dense<false>;
   static int per_sm = 0;
   if (!per_sm) BBTC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_dense<true>, kWarps * 32, 0));
   const int per = std::max(1, std::min(per_sm, kCtasPerSm));

@@ -1348,6 +1348,9 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       // Few blocks: sort each block in place by its local column (no key pass).  With
       // row bands (BBTC_BANDS=1) the key is (row band, column): a block whose probe blocks
       // G_ik (k >= j) exceed BBTC_BAND_BYTES (default 32 MB) is walked band by band.
+      // Measured slower (friendster p=4 list kernel 333 ms -> 440 / 565 / 740 ms at 64 /
+      // 32 / 16 MB bands: every band re-reads the staged lists of the columns it
+      // touches), so it stays an option.
       static const bool bands = getenv("BBTC_BANDS") != nullptr;
       static const double band_bytes = getenv("BBTC_BAND_BYTES") ? atof(getenv("BBTC_BAND_BYTES")) : 32e6;
       plan->band_shift.assign(nb, -1);
