@@ -225,6 +225,11 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
     for (uint32_t i = 0; i < p; ++i)
       for (uint32_t j = i; j < p; ++j)
         for (uint32_t k = j; k < p; ++k) order.push_back({i, j, k});
+  } else if (oe && std::string(oe) == "ikj") {
+    // probe block G_ik fixed in the inner loop (its random gathers can stay in L2)
+    for (uint32_t i = 0; i < p; ++i)
+      for (uint32_t k = i; k < p; ++k)
+        for (uint32_t j = i; j <= k; ++j) order.push_back({i, j, k});
   } else if (oe && std::string(oe) == "kdesc") {
     for (uint32_t k = p; k-- > 0;)
       for (uint32_t j = 0; j <= k; ++j)
