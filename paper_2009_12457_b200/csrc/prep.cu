@@ -105,7 +105,11 @@ __global__ void k_degree_any(const uint64_t* __restrict__ keys, uint64_t m, int 
 }
 
 // ---- a2 ------------------------------------------------------------------------------
-__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, int bw, uint32_t* __restrict__ deg) {
+// Degrees of sorted unique keys.  The lo side (sorted) is aggregated per warp; the hi
+// side is random, so it can be split into passes over id ranges [h0, h1) small enough
+// for the L2 (degrees_sorted below): the lo side is counted in the first pass only.
+__global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, int bw, uint32_t* __restrict__ deg,
+                         uint32_t h0 = 0, uint32_t h1 = 0xFFFFFFFFu, bool with_lo = true) {
   // Warp-uniform trip count so the whole warp stays converged for __match_any_sync.
   const uint64_t lane = threadIdx.x & 31;
   const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane;
@@ -116,10 +120,11 @@ __global__ void k_degree(const uint64_t* __restrict__ keys, uint64_t m, int bw, 
     const uint64_t k = valid ? keys[e] : 0;
     const uint32_t lo = valid ? (uint32_t)(k >> bw) : 0xFFFFFFFFu;
     const uint32_t hi = (uint32_t)(k & ((1ull << bw) - 1));
-    // Keys are sorted, so equal `lo` values sit in the same warp: aggregate them.
-    const uint32_t peers = __match_any_sync(0xffffffffu, lo);
-    if (valid && lane == (uint64_t)(__ffs(peers) - 1)) atomicAdd(&deg[lo], __popc(peers));
-    if (valid) atomicAdd(&deg[hi], 1u);
+    if (with_lo) {   // keys are sorted, so equal `lo` values sit in the same warp: aggregate them
+      const uint32_t peers = __match_any_sync(0xffffffffu, lo);
+      if (valid && lane == (uint64_t)(__ffs(peers) - 1)) atomicAdd(&deg[lo], __popc(peers));
+    }
+    if (valid && hi >= h0 && hi < h1) atomicAdd(&deg[hi], 1u);
   }
 }
 
@@ -132,11 +137,14 @@ __global__ void k_rank(const uint32_t* __restrict__ order, uint32_t n, uint32_t*
 }
 
 // Orientation from lower to higher degree rank (P:226-235 with the order of P:438-446).
+// [h0, h1): only keys whose hi id falls in it (passes over L2-sized slices of rank[]).
 __global__ void k_orient(const uint64_t* __restrict__ keys, uint64_t m, int bw, const uint32_t* __restrict__ rank,
-                         uint64_t* __restrict__ okeys) {
+                         uint64_t* __restrict__ okeys, uint32_t h0 = 0, uint32_t h1 = 0xFFFFFFFFu) {
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[e];
-    uint32_t ra = rank[(uint32_t)(k >> bw)], rb = rank[(uint32_t)(k & ((1ull << bw) - 1))];
+    const uint32_t hi = (uint32_t)(k & ((1ull << bw) - 1));
+    if (hi < h0 || hi >= h1) continue;
+    uint32_t ra = rank[(uint32_t)(k >> bw)], rb = rank[hi];
     okeys[e] = ((uint64_t)min(ra, rb) << 32) | max(ra, rb);
   }
 }
@@ -742,6 +750,34 @@ __global__ void k_narrow(uint64_t* __restrict__ keys, uint64_t m, int bw) {
 
 }  // namespace
 
+// Passes over id slices for the random (hi-side) accesses of the degree count and the
+// orientation: one slice of the n-entry array per pass, sized to a share of the L2
+// (BBTC_L2_SLICE_MB, default 48 MB) — friendster (n = 65.6 M, 262 MB arrays) takes 6
+// passes, each re-reading the keys sequentially but hitting L2 on the gathers.
+static uint32_t id_slices(uint32_t n) {
+  static const double mb = getenv("BBTC_L2_SLICE_MB") ? atof(getenv("BBTC_L2_SLICE_MB")) : 48.0;
+  const double bytes = 4.0 * n;
+  if (mb <= 0 || bytes <= 100e6) return 1;   // (fits the 126 MB L2 well enough: rmat24's 67 MB)
+  return std::max<uint32_t>(1, (uint32_t)std::ceil(bytes / (mb * 1e6)));
+}
+static void degrees_sorted(bbtc_ctx* ctx, const uint64_t* keys, uint64_t m, int bw, uint32_t n, uint32_t* deg) {
+  const uint32_t q = id_slices(n);
+  for (uint32_t x = 0; x < q; ++x) {
+    const uint32_t h0 = (uint32_t)((uint64_t)n * x / q), h1 = (uint32_t)((uint64_t)n * (x + 1) / q);
+    k_degree<<<grid_for(ctx, m), kThreads, 0, ctx->stream>>>(keys, m, bw, deg, h0, q == 1 ? 0xFFFFFFFFu : h1, x == 0);
+    BBTC_LAUNCHED(ctx);
+  }
+}
+static void orient_sliced(bbtc_ctx* ctx, const uint64_t* keys, uint64_t m, int bw, uint32_t n, const uint32_t* rank,
+                          uint64_t* okeys) {
+  const uint32_t q = id_slices(n);
+  for (uint32_t x = 0; x < q; ++x) {
+    const uint32_t h0 = (uint32_t)((uint64_t)n * x / q), h1 = (uint32_t)((uint64_t)n * (x + 1) / q);
+    k_orient<<<grid_for(ctx, m), kThreads, 0, ctx->stream>>>(keys, m, bw, rank, okeys, h0, q == 1 ? 0xFFFFFFFFu : h1);
+    BBTC_LAUNCHED(ctx);
+  }
+}
+
 // a1 bucket de-duplication of keys[0, E) (K live bits; sentinels skipped), BBTC_BUCKET=1:
 // measured slower than the onesweep sort + unique on B200 (rmat24 20.2 vs 17.5 ms, and
 // the unsorted keys cost the degree pass 6.4 vs 2.5 ms), kept as an option.  Returns
@@ -1038,8 +1074,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       k_degree_any<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
       BBTC_LAUNCHED(ctx);
     } else if (m) {
-      k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, deg.p);
-      BBTC_LAUNCHED(ctx);
+      degrees_sorted(ctx, ukeys.p, m, bw, n, deg.p);
     }
     tr.mark("degree");
     DevBuf<uint32_t> ids, order;
@@ -1055,8 +1090,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     BBTC_LAUNCHED(ctx);
     tr.mark("rank");
     if (m) {
-      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(ukeys.p, m, bw, g->rank.p, g->okeys.p);
-      BBTC_LAUNCHED(ctx);
+      orient_sliced(ctx, ukeys.p, m, bw, n, g->rank.p, g->okeys.p);
     }
     tr.mark("orient");
     k_graph_stats<<<1, 32, 0, st>>>(g->deg_sorted.p, n, dmax.p);
