@@ -1753,10 +1753,7 @@ void shard_graph(bbtc_ctx* ctx, const uint64_t* wire, uint64_t cnt, uint32_t n, 
   g->cbw = bw;
   g->ckeys = std::move(keys);
   BBTC_CUDA(cudaMemsetAsync(d_deg, 0, (size_t)n * 4, st));
-  if (m) {
-    k_degree<<<grid_for(ctx, m), kThreads, 0, st>>>(g->ckeys.p, m, bw, d_deg);
-    BBTC_LAUNCHED(ctx);
-  }
+  if (m) degrees_sorted(ctx, g->ckeys.p, m, bw, n, d_deg);
   tr.mark("degree");
 }
 
@@ -1782,10 +1779,7 @@ void shard_rank(bbtc_ctx* ctx, bbtc_graph* g, const uint32_t* d_deg, uint64_t m_
     }, radix_kernels(n, bdeg));
     k_rank<<<grid_for(ctx, n), kThreads, 0, st>>>(order.p, n, g->rank.p);
     BBTC_LAUNCHED(ctx);
-    if (m) {
-      k_orient<<<grid_for(ctx, m), kThreads, 0, st>>>(g->ckeys.p, m, g->cbw, g->rank.p, g->okeys.p);
-      BBTC_LAUNCHED(ctx);
-    }
+    if (m) orient_sliced(ctx, g->ckeys.p, m, g->cbw, n, g->rank.p, g->okeys.p);
     k_graph_stats<<<1, 32, 0, st>>>(g->deg_sorted.p, n, dmax.p);
     BBTC_LAUNCHED(ctx);
     uint32_t h[2];
