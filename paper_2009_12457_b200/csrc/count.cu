@@ -59,6 +59,9 @@ constexpr bool kRunPipe = BBTC_RUN_PIPE;   // pipelined column runs (hash-only v
 // friendster unchanged (profiles/r02/ab5; K = 3 / always: no better, friendster worse).
 #define BBTC_LANEWALK 1
 #endif
+#ifndef BBTC_TAIL3
+#define BBTC_TAIL3 0   // A/B: the last < 4 rounds of a long probe list with all loads in flight
+#endif
 #ifndef BBTC_LANEWALK_K
 #define BBTC_LANEWALK_K 2  // lane walk when 32 * max remainder <= K * sum of remainders + 64
 #endif
@@ -165,7 +168,17 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
       const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
       hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
     }
+#if BBTC_TAIL3
+    // the last 0-3 full rounds with their loads issued together (lists of 32-127 words
+    // otherwise wait out one load latency per round)
+    const uint32_t nr = (nfull - off) >> 5;
+    const uint32_t t1 = nr > 0 ? B[off] : 0u, t2 = nr > 1 ? B[off + 32] : 0u, t3 = nr > 2 ? B[off + 64] : 0u;
+    if (nr > 0) hits += test(t1, sl);
+    if (nr > 1) hits += test(t2, sl);
+    if (nr > 2) hits += test(t3, sl);
+#else
     for (; off < nfull; off += 32) hits += test(B[off], sl);
+#endif
   }
   const uint32_t rem = bl & 31u;
 #if BBTC_LANEWALK
