@@ -1,0 +1,5 @@
+#!/bin/bash
+out=gpurun_out/${OUT:-ab7}; mkdir -p $out
+timeout 2400 python scripts/ab_variants.py rmat24:10,orkut,friendster paper_2009_12457_b200/libbbtc.so build_ab/tail3/libbbtc.so > $out/ab_tail3.jsonl 2>> $out/err.txt
+timeout 2400 python scripts/ab_variants.py rmat24:10,orkut paper_2009_12457_b200/libbbtc.so build_ab/tail3/libbbtc.so >> $out/ab_tail3.jsonl 2>> $out/err.txt
+echo done >> $out/steps.txt
