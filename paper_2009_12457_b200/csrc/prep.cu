@@ -750,10 +750,10 @@ __global__ void k_narrow(uint64_t* __restrict__ keys, uint64_t m, int bw) {
 
 }  // namespace
 
-// Passes over id slices for the random (hi-side) accesses of the degree count and the
-// orientation: one slice of the n-entry array per pass, sized to a share of the L2
-// (BBTC_L2_SLICE_MB, default 48 MB) — friendster (n = 65.6 M, 262 MB arrays) takes 6
-// passes, each re-reading the keys sequentially but hitting L2 on the gathers.
+// Passes over id slices for the random (hi-side) atomics of the degree count: one
+// slice of the n-entry array per pass, sized to a share of the L2 (BBTC_L2_SLICE_MB,
+// default 48 MB) — friendster (n = 65.6 M, 262 MB) takes 6 passes, each re-reading the
+// keys sequentially but keeping the atomics in L2: 42.7 -> 24.5 ms.
 static uint32_t id_slices(uint32_t n) {
   static const double mb = getenv("BBTC_L2_SLICE_MB") ? atof(getenv("BBTC_L2_SLICE_MB")) : 48.0;
   const double bytes = 4.0 * n;
@@ -768,9 +768,12 @@ static void degrees_sorted(bbtc_ctx* ctx, const uint64_t* keys, uint64_t m, int 
     BBTC_LAUNCHED(ctx);
   }
 }
+// (Slicing the orientation measured slower — friendster 24.2 -> 33.2 ms: it reads and
+// writes 16 B per key per pass against one 4 B gather — so it runs in one pass unless
+// BBTC_ORIENT_SLICES=1.)
 static void orient_sliced(bbtc_ctx* ctx, const uint64_t* keys, uint64_t m, int bw, uint32_t n, const uint32_t* rank,
                           uint64_t* okeys) {
-  const uint32_t q = id_slices(n);
+  const uint32_t q = getenv("BBTC_ORIENT_SLICES") ? id_slices(n) : 1;
   for (uint32_t x = 0; x < q; ++x) {
     const uint32_t h0 = (uint32_t)((uint64_t)n * x / q), h1 = (uint32_t)((uint64_t)n * (x + 1) / q);
     k_orient<<<grid_for(ctx, m), kThreads, 0, ctx->stream>>>(keys, m, bw, rank, okeys, h0, q == 1 ? 0xFFFFFFFFu : h1);
