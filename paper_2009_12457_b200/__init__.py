@@ -11,6 +11,7 @@ partition, BCSR, count) runs in the library's sm_100a kernels.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import weakref
 
@@ -70,6 +71,20 @@ def task_ijk(p: int, idx: int):
     return int(i.value), int(j.value), int(k.value)
 
 
+_LIVE = weakref.WeakSet()   # live contexts
+
+
+@atexit.register
+def _close_all():
+    """Free every live context (and its graphs and plans) while the interpreter and the
+    CUDA runtime are intact — not in arbitrary order during module teardown."""
+    for c in list(_LIVE):
+        try:
+            c.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class Context:
     """A CUDA device + the stream the library enqueues on (bbtc_ctx)."""
 
@@ -85,6 +100,7 @@ class Context:
         self._h = h
         self.device = device
         self._children = weakref.WeakSet()   # graphs / plans: freed before the context
+        _LIVE.add(self)
 
     @property
     def handle(self):
