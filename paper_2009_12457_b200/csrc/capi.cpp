@@ -1125,6 +1125,34 @@ static const DevArenas* ab_colptr_arenas(bbtc_plan* plan, DevArenas* ar) {
 // kernel over the dense tasks' items (building the bit rows on first use).
 static void count_resident(bbtc_ctx* ctx, bbtc_plan* plan, uint32_t rank, uint32_t world, uint64_t* d_counts,
                            cudaEvent_t mid = nullptr) {
+  static const bool concurrent = getenv("BBTC_DENSE_CONCURRENT") != nullptr;
+  if (concurrent && !mid && plan->dense_item_lo < plan->item_start.back()) {
+    // A/B: the bit-row build and kernel on the aux stream beside the list kernel (they
+    // share only the counters, updated atomically): the dense CTAs take SMs as the
+    // persistent list kernel's CTAs retire.
+    cudaEvent_t go, done;
+    BBTC_CUDA(cudaEventCreateWithFlags(&go, cudaEventDisableTiming));
+    BBTC_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    BBTC_CUDA(cudaEventRecord(go, ctx->stream));
+    BBTC_CUDA(cudaStreamWaitEvent(ctx->aux_stream, go, 0));
+    cudaStream_t main_st = ctx->stream;
+    ctx->stream = ctx->aux_stream;
+    try {
+      dense_build(ctx, plan);
+      count_launch_dense(ctx, plan, rank, world, d_counts, plan->dense_item_lo, plan->item_start.back());
+    } catch (...) {
+      ctx->stream = main_st;
+      throw;
+    }
+    ctx->stream = main_st;
+    BBTC_CUDA(cudaEventRecord(done, ctx->aux_stream));
+    DevArenas ar;
+    count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0, ab_colptr_arenas(plan, &ar));
+    BBTC_CUDA(cudaStreamWaitEvent(ctx->stream, done, 0));
+    cudaEventDestroy(go);
+    cudaEventDestroy(done);
+    return;
+  }
   dense_build(ctx, plan);
   DevArenas ar;
   count_launch(ctx, plan, rank, world, d_counts, 0, plan->dense_item_lo, nullptr, 0, ab_colptr_arenas(plan, &ar));
