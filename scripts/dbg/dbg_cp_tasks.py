@@ -1,7 +1,7 @@
 """Which tasks does the column-offset walk (kCP) slow down?  Per-task times with and
 without BBTC_FORCE_CP on the same staged host plan."""
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import inputs, paper_2009_12457_b200 as bb

@@ -1,7 +1,7 @@
 """Which dense (bit-row) tasks carry the bit-row kernel's time: per-task warp time
 (bbtc_task_times) with block sizes and G_ij density."""
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np
 import inputs, paper_2009_12457_b200 as bb

@@ -1,6 +1,6 @@
 """Exit-time teardown check: module-level context, graph, plan alive at exit."""
 import os, sys
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import inputs, paper_2009_12457_b200 as bb
 s, d = inputs.rmat(16, 16, 1)
