@@ -1516,7 +1516,7 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
     const uint32_t w = plan->cuts[B.j + 1] - plan->cuts[B.j];
     // (>= 4 edges per column on average: with sparser columns the kernel's 32-column
     // windows cover too few edges per batch — rmat24 (1,1): 2 edges/column, the
-    // column-offset walk 2.7x slower than reading ccv, scripts/dbg_cp_tasks.py)
+    // column-offset walk 2.7x slower than reading ccv, scripts/dbg/dbg_cp_tasks.py)
     const bool cp = B.nnz >= 4 * ((uint64_t)w + 1) &&
                     (plan->band_shift.empty() || plan->band_shift[b] < 0);   // (a banded column is split)
     if (cp) {
