@@ -59,6 +59,19 @@ constexpr bool kRunPipe = BBTC_RUN_PIPE;   // pipelined column runs (hash-only v
 // friendster unchanged (profiles/r02/ab5; K = 3 / always: no better, friendster worse).
 #define BBTC_LANEWALK 1
 #endif
+#ifndef BBTC_STREAM_HINT
+#define BBTC_STREAM_HINT 0   // A/B: evict-first (ld.global.cs) loads for the walked edges and staged lists
+#endif
+// Loads of data read once in order (the walk arrays, the staged lists): with the hint
+// they are marked evict-first so the L2 keeps the randomly gathered probe lists.
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#if BBTC_STREAM_HINT
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
 #ifndef BBTC_TAIL3
 #define BBTC_TAIL3 0   // A/B: the last < 4 rounds of a long probe list with all loads in flight
 #endif
@@ -229,7 +242,7 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
     const int shift = 32 - (__ffs(nb) - 1);
     for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
-    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, cS[s0 + c0 + x], shift, bmask);
+    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, ld_stream(cS + s0 + c0 + x), shift, bmask);
     __syncwarp();
     hits += probe_lists(cols, pay, lane, bx, bl, 0,
                         [&](uint32_t w, uint32_t) { return table_probe(tab4, w, shift, bmask); });
@@ -373,10 +386,10 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       // ---- 32 edges (u,v) of G_ij; key = the staged side's row (v by column, u by row)
       const uint64_t e = base + lane;
       const bool valid = e < e_end;
-      const uint32_t u = valid ? it_u[e] : 0xFFFFFFFFu;
+      const uint32_t u = valid ? ld_stream(it_u + e) : 0xFFFFFFFFu;
       uint32_t v;
       if (cpm) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
-      else v = valid ? it_v[e] : 0xFFFFFFFFu;
+      else v = valid ? ld_stream(it_v + e) : 0xFFFFFFFFu;
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
       uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;   // a: staged list, b: probe list
@@ -432,7 +445,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         if (L == 32 && __all_sync(kFull, valid && key == k0)) {
           // kCP: the run's edges end where column k0 ends
           const uint64_t run_end = cpm ? Bij.e0 + cpb[k0 + 1] : 0;
-          auto same = [&](uint64_t e) { return cpm ? e < run_end : (kCol ? it_v[e] : it_u[e]) == k0; };
+          auto same = [&](uint64_t e) { return cpm ? e < run_end : ld_stream((kCol ? it_v : it_u) + e) == k0; };
           if constexpr (kRunPipe && (!kBm || BBTC_RUN_PIPE_BM)) {
             // Two-stage pipeline over the run's batches: while batch t is probed, the row
             // offsets of batch t+1 (whose edge ids arrived during batch t-1) and the edge
@@ -441,7 +454,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
             // rmat24 (profiles/r01c/ab_run_pipe.jsonl).
             auto edge = [&](uint64_t e, uint32_t& pid2) {
               const bool ok = e < e_end && same(e);
-              pid2 = ok ? (kCol ? it_u[e] : it_v[e]) : 0u;
+              pid2 = ok ? ld_stream((kCol ? it_u : it_v) + e) : 0u;
               return ok;
             };
             uint64_t e2 = base + L + lane;
@@ -504,12 +517,12 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           if (lmask == 1u) {   // one list: coalesced reads, no flattening
             const uint32_t s0 = __shfl_sync(kFull, a0, 0), sn = __shfl_sync(kFull, alen, 0);
             for (uint32_t x = lane; x < sn; x += 32) {
-              const uint32_t w = cS[s0 + x];
+              const uint32_t w = ld_stream(cS + s0 + x);
               atomicOr(bm + (w >> 5), 1u << (w & 31));
             }
           } else {
             flatten(pay, lane, leader && alen > 0, aoff, make_uint2(a0 - aoff, slot * bmw),
-                    __shfl_sync(kFull, aend, L - 1), [&](uint32_t f, uint2 P) { return cS[P.x + f]; },
+                    __shfl_sync(kFull, aend, L - 1), [&](uint32_t f, uint2 P) { return ld_stream(cS + P.x + f); },
                     [&](uint32_t, uint2 P, uint32_t w) { atomicOr(bm + P.y + (w >> 5), 1u << (w & 31)); });
           }
           __syncwarp();
@@ -529,7 +542,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint2(a0 - aoff, slot), total_a,
-                  [&](uint32_t f, uint2 P) { return cS[P.x + f]; },
+                  [&](uint32_t f, uint2 P) { return ld_stream(cS + P.x + f); },
                   [&](uint32_t, uint2 P, uint32_t w) { table_insert(tab, (w << 5) | P.y, shift, bmask); });
           // ---- probe every word of each lane's list P against its staged list
           auto test = [&](uint32_t w, uint32_t sl) { return table_probe(tab4, (w << 5) | sl, shift, bmask); };
