@@ -1477,7 +1477,16 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     // |V_i| for i < j, so more of them stay in L2 (rmat24 p=10: 13.2 -> 11.4 ms;
     // BBTC_DENSE_WALK=col walks by column as in round 1).
     const char* dw = getenv("BBTC_DENSE_WALK");
-    if ((dw && std::string(dw) == "col") || (flags & BBTC_PLAN_SPARSE)) plan->rows.reset();
+    bool maybe_dense = false;   // some part small enough for bit rows (else no dense task can exist)
+    {
+      const char* e = getenv("BBTC_DENSE_BITS");
+      const uint32_t bits = e ? (uint32_t)atoi(e) : kDenseBitsDefault;
+      for (uint32_t k = 0; k < pe; ++k) {
+        const uint32_t vk = plan->cuts[k + 1] - plan->cuts[k];
+        maybe_dense = maybe_dense || (vk > 0 && vk <= std::min(bits, kDenseMaxS * 32));
+      }
+    }
+    if ((dw && std::string(dw) == "col") || (flags & BBTC_PLAN_SPARSE) || !maybe_dense) plan->rows.reset();
     bytes += 4 * m;       // cols + ccu + ccv instead of cols + rows
     tr.mark("transpose");
   }
