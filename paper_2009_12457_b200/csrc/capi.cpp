@@ -389,7 +389,8 @@ void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32
   std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.w > b.w || (a.w == b.w && a.idx < b.idx); });
   std::vector<double> load(world, 0.0);
   std::vector<std::vector<char>> has(world, std::vector<char>(nb, 0));
-  const double share = total / world * 1.02;
+  static const double slack = getenv("BBTC_LPT_SLACK") ? atof(getenv("BBTC_LPT_SLACK")) : 1.02;
+  const double share = total / world * slack;
   for (const T& t : ts) {
     const uint32_t bl[3] = {block_id(t.i, t.j), block_id(t.i, t.k), block_id(t.j, t.k)};
     const uint32_t bi[3] = {t.i, t.i, t.j};
