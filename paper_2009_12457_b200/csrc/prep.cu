@@ -1325,7 +1325,8 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     const int kb = bitlen(nb - 1);
     // The batched path keeps every block's first edge in shared memory (8 B each).
     const size_t key_smem = (size_t)nb * 8;
-    const bool batched = nb > 36 && key_smem <= 200 * 1024;
+    static const uint32_t batched_min = getenv("BBTC_BATCHED_MIN_NB") ? (uint32_t)atoi(getenv("BBTC_BATCHED_MIN_NB")) : 37;
+    const bool batched = nb >= batched_min && key_smem <= 200 * 1024;
     // Packed keys: cbase[b] = Σ over earlier blocks of their live column widths.
     const uint32_t n_iso = g->n - g->n_nonisolated;   // isolated vertices: ranks [0, n_iso)
     std::vector<uint32_t> trim(pe), cbase(nb);
