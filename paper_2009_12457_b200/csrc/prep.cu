@@ -1325,7 +1325,10 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     const int kb = bitlen(nb - 1);
     // The batched path keeps every block's first edge in shared memory (8 B each).
     const size_t key_smem = (size_t)nb * 8;
-    static const uint32_t batched_min = getenv("BBTC_BATCHED_MIN_NB") ? (uint32_t)atoi(getenv("BBTC_BATCHED_MIN_NB")) : 37;
+    // One batched sort from 16 blocks (p >= 6) on, per-block sorts below: orkut p=8 (36
+    // blocks) plan 9.98 -> 9.15 ms batched; friendster p=4 (10 blocks) 130.5 vs 148.3 ms
+    // per-block (profiles/r02/ab10).
+    static const uint32_t batched_min = getenv("BBTC_BATCHED_MIN_NB") ? (uint32_t)atoi(getenv("BBTC_BATCHED_MIN_NB")) : 16;
     const bool batched = nb >= batched_min && key_smem <= 200 * 1024;
     // Packed keys: cbase[b] = Σ over earlier blocks of their live column widths.
     const uint32_t n_iso = g->n - g->n_nonisolated;   // isolated vertices: ranks [0, n_iso)
