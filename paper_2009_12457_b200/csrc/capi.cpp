@@ -654,6 +654,10 @@ BBTC_API bbtc_status bbtc_ctx_create(const bbtc_ctx_opts* opts, bbtc_ctx** out) 
       c->copy_streams.push_back(s);
     }
     BBTC_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    // A/B knob: the L2's DRAM fetch granularity for misses (32/64/128 B; the random
+    // row-offset and probe-list gathers use a few words of each fetched line).
+    if (const char* fg = getenv("BBTC_L2_FETCH"))
+      BBTC_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg)));
     // Keep freed pool memory cached between steps (no OS round trips per call).
     cudaMemPool_t pool;
     BBTC_CUDA(cudaDeviceGetDefaultMemPool(&pool, o.device));

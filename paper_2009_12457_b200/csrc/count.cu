@@ -72,6 +72,12 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return *p;
 #endif
 }
+#ifndef BBTC_P1_DEPTH
+#define BBTC_P1_DEPTH 4   // A/B: 8 = rounds of eight 32-word loads in flight for long probe lists
+#endif
+#ifndef BBTC_PF_NEXT
+#define BBTC_PF_NEXT 0   // A/B: rolling L2 prefetch of the next long probe list and of the remainders
+#endif
 #ifndef BBTC_TAIL3
 #define BBTC_TAIL3 0   // A/B: the last < 4 rounds of a long probe list with all loads in flight
 #endif
@@ -88,6 +94,11 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
   }
   return x;
 }
+
+// Length of the run of set bits from lane 0.  Equal staged keys are contiguous in a
+// column-ordered block, but not in a row-banded one (a column reappears in the next
+// band): a batch or run takes only the leading lanes of its key.
+__device__ __forceinline__ int lane_prefix(uint32_t b) { return b == kFull ? 32 : __ffs(~b) - 1; }
 
 __device__ __forceinline__ uint32_t lanemask_le(int lane) { return 0xffffffffu >> (31 - lane); }
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -136,29 +147,64 @@ __device__ __forceinline__ void flatten(uint2* pay, int lane, bool nonempty, uin
   __syncwarp();
 }
 
-// Inserts key hk into the table of 4-word buckets (linear probing over buckets).
-__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t hk, int shift, uint32_t bmask) {
-  uint32_t h = hbucket(hk, shift);
+// Buckets of kBW words (BBTC_BUCKET_WORDS; 4 by default: one LDS.128 per probe).  A
+// table is sized in 4-word units (nb4 of them) and addressed in buckets of kBW words.
+#ifndef BBTC_BUCKET_WORDS
+#define BBTC_BUCKET_WORDS 4
+#endif
+constexpr int kBW = BBTC_BUCKET_WORDS;
+static_assert(kBW == 1 || kBW == 2 || kBW == 4, "bucket width");
+struct TabGeom {
+  uint32_t bmask;
+  int shift;
+};
+__device__ __forceinline__ TabGeom tab_geom(uint32_t nb4) {
+  const uint32_t nb = nb4 * (4 / kBW);
+  return {nb - 1, 32 - (__ffs(nb) - 1)};
+}
+
+// Inserts key hk into the table (linear probing over buckets).
+__device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t hk, TabGeom G) {
+  uint32_t h = hbucket(hk, G.shift);
   for (;;) {
-    uint32_t* bk = tab + 4 * h;
-    if (atomicCAS(bk + 0, kEmpty, hk) == kEmpty) return;
-    if (atomicCAS(bk + 1, kEmpty, hk) == kEmpty) return;
-    if (atomicCAS(bk + 2, kEmpty, hk) == kEmpty) return;
-    if (atomicCAS(bk + 3, kEmpty, hk) == kEmpty) return;
-    h = (h + 1) & bmask;
+    uint32_t* bk = tab + kBW * h;
+#pragma unroll
+    for (int x = 0; x < kBW; ++x)
+      if (atomicCAS(bk + x, kEmpty, hk) == kEmpty) return;
+    h = (h + 1) & G.bmask;
   }
 }
 
-__device__ __forceinline__ uint32_t table_probe(const uint4* tab4, uint32_t hk, int shift, uint32_t bmask) {
-  uint32_t h = hbucket(hk, shift);
-  uint4 q = tab4[h];
-  bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
-  while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at these loads)
-    h = (h + 1) & bmask;
-    q = tab4[h];
-    hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
+__device__ __forceinline__ uint32_t table_probe(const uint32_t* tab, uint32_t hk, TabGeom G) {
+  uint32_t h = hbucket(hk, G.shift);
+  if constexpr (kBW == 4) {
+    const uint4* tab4 = reinterpret_cast<const uint4*>(tab);
+    uint4 q = tab4[h];
+    bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
+    while (!hit && q.w != kEmpty) {   // full bucket: next one (rare at these loads)
+      h = (h + 1) & G.bmask;
+      q = tab4[h];
+      hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
+    }
+    return hit;
+  } else if constexpr (kBW == 2) {
+    const uint2* tab2 = reinterpret_cast<const uint2*>(tab);
+    uint2 q = tab2[h];
+    bool hit = (q.x == hk) | (q.y == hk);
+    while (!hit && q.y != kEmpty) {
+      h = (h + 1) & G.bmask;
+      q = tab2[h];
+      hit = (q.x == hk) | (q.y == hk);
+    }
+    return hit;
+  } else {
+    uint32_t q = tab[h];
+    while (q != hk && q != kEmpty) {
+      h = (h + 1) & G.bmask;
+      q = tab[h];
+    }
+    return q == hk;
   }
-  return hit;
 }
 
 // Probe lists of lanes: P = cols[bx .. bx + bl).  Phase 1 walks the long lists one at
@@ -170,13 +216,40 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
                                                 uint32_t bl, uint32_t slot, Test test) {
   uint32_t hits = 0;
   uint32_t longs = __ballot_sync(kFull, bl >= 32);
+#if BBTC_PF_NEXT
+  // Rolling L2 prefetch: every lane asks for its own < 32-word remainder now (phase 2
+  // reads it after all long lists), and the lines of the next long list are requested
+  // while the current one is walked, so each list's first round finds it in L2.
+  if (bl & 31u) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + bx + (bl & ~31u)));
+  if (longs) {
+    const int s0 = __ffs(longs) - 1;
+    const uint32_t n0 = __shfl_sync(kFull, bl, s0), x0 = __shfl_sync(kFull, bx, s0);
+    if (32 * lane < n0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + x0 + 32 * lane));
+  }
+#endif
   while (longs) {
     const int src = __ffs(longs) - 1;
     longs &= longs - 1;
+#if BBTC_PF_NEXT
+    if (longs) {
+      const int s1 = __ffs(longs) - 1;
+      const uint32_t n1 = __shfl_sync(kFull, bl, s1), x1 = __shfl_sync(kFull, bx, s1);
+      if (32 * lane < n1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + x1 + 32 * lane));
+    }
+#endif
     const uint32_t* B = cols + __shfl_sync(kFull, bx, src) + lane;
     const uint32_t nfull = __shfl_sync(kFull, bl, src) & ~31u;
     const uint32_t sl = __shfl_sync(kFull, slot, src);
     uint32_t off = 0;
+#if BBTC_P1_DEPTH == 8
+    for (; off + 256 <= nfull; off += 256) {
+      uint32_t w[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) w[x] = B[off + 32 * x];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) hits += test(w[x], sl);
+    }
+#endif
     for (; off + 128 <= nfull; off += 128) {
       const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
       hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
@@ -238,14 +311,13 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
     const uint32_t cn = min((uint32_t)kChunk, total_a - c0);
     uint32_t nb = 16;
     while (2 * nb < cn) nb <<= 1;
-    const uint32_t bmask = nb - 1;
-    const int shift = 32 - (__ffs(nb) - 1);
+    const TabGeom G = tab_geom(nb);
     for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
-    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, ld_stream(cS + s0 + c0 + x), shift, bmask);
+    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, ld_stream(cS + s0 + c0 + x), G);
     __syncwarp();
     hits += probe_lists(cols, pay, lane, bx, bl, 0,
-                        [&](uint32_t w, uint32_t) { return table_probe(tab4, w, shift, bmask); });
+                        [&](uint32_t w, uint32_t) { return table_probe(tab, w, G); });
   }
   return hits;
 }
@@ -421,7 +493,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       if (L == 0) {
         const uint32_t k0 = __shfl_sync(kFull, key, 0);
         const uint32_t a_first = __shfl_sync(kFull, alen, 0);
-        L = __popc(__ballot_sync(kFull, valid && key == k0));
+        L = lane_prefix(__ballot_sync(kFull, valid && key == k0));
         if (kSlots && a_first <= kChunk) dense = true;
         else longl = true;
       }
@@ -467,7 +539,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
               bl2 = rpP[p_cur + 1] - b2;
             }
             for (;;) {
-              const int L2 = __popc(__ballot_sync(kFull, ok_cur));   // the run's edges: a lane prefix
+              const int L2 = lane_prefix(__ballot_sync(kFull, ok_cur));   // the run's edges
               if (L2 == 0) break;
               uint32_t bn = 0, bln = 0, p_nn = 0;
               bool ok_nn = false;
@@ -478,7 +550,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                 }
                 ok_nn = edge(e2 + 64, p_nn);
               }
-              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
+              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
               e2 += 32;
@@ -492,7 +564,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
             for (;;) {
               const uint64_t e2 = base + L + lane;
               const bool ok = e2 < e_end && same(e2);
-              const int L2 = __popc(__ballot_sync(kFull, ok));   // the run's edges: a lane prefix
+              const int L2 = lane_prefix(__ballot_sync(kFull, ok));   // the run's edges
               if (L2 == 0) break;
               uint32_t b2 = 0, bl2 = 0;
               if (ok && alen > 0) {
@@ -500,7 +572,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                 b2 = rpP[p2];
                 bl2 = rpP[p2 + 1] - b2;
               }
-              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, bl2, 0, test);
+              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
           }
@@ -537,15 +609,14 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
           uint32_t nb = 16;
           while ((dense || kLoadHalf ? 2 * nb : nb) < total_a) nb <<= 1;
-          const uint32_t bmask = nb - 1;
-          const int shift = 32 - (__ffs(nb) - 1);
+          const TabGeom G = tab_geom(nb);
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint2(a0 - aoff, slot), total_a,
                   [&](uint32_t f, uint2 P) { return ld_stream(cS + P.x + f); },
-                  [&](uint32_t, uint2 P, uint32_t w) { table_insert(tab, (w << 5) | P.y, shift, bmask); });
+                  [&](uint32_t, uint2 P, uint32_t w) { table_insert(tab, (w << 5) | P.y, G); });
           // ---- probe every word of each lane's list P against its staged list
-          auto test = [&](uint32_t w, uint32_t sl) { return table_probe(tab4, (w << 5) | sl, shift, bmask); };
+          auto test = [&](uint32_t w, uint32_t sl) { return table_probe(tab, (w << 5) | sl, G); };
           hits += probe_lists(cols, pay, lane, bx, bl, slot, test);
           continue_run(test);
         }

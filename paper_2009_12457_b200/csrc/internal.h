@@ -25,9 +25,14 @@ struct Error {
       ::bbtc::raise(e_ == cudaErrorMemoryAllocation ? BBTC_ENOMEM : BBTC_ECUDA,                \
                     std::string(#call) + ": " + cudaGetErrorString(e_));                       \
   } while (0)
+#define BBTC_STR2_(x) #x
+#define BBTC_STR_(x) BBTC_STR2_(x)
 #define BBTC_LAUNCHED(ctx)                                                                     \
   do {                                                                                         \
-    BBTC_CUDA(cudaGetLastError());                                                             \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess)                                                                     \
+      ::bbtc::raise(BBTC_ECUDA, std::string("kernel launched at " __FILE__ ":" BBTC_STR_(__LINE__) ": ") + \
+                                    cudaGetErrorString(e_));                                   \
     (ctx)->launches++;                                                                         \
   } while (0)
 

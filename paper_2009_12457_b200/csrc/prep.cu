@@ -1392,7 +1392,14 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       // Measured slower (friendster p=4 list kernel 333 ms -> 440 / 565 / 740 ms at 64 /
       // 32 / 16 MB bands: every band re-reads the staged lists of the columns it
       // touches), so it stays an option.
-      static const bool bands = getenv("BBTC_BANDS") != nullptr;
+      // BBTC_BANDS=all bands every such block; BBTC_BANDS=cost only blocks whose tasks'
+      // probe words (nnz_ij x δ(G_ik), summed over k) exceed BBTC_BAND_RATIO (default 4)
+      // times the staged words the bands re-read (bands x non-empty columns x δ(G_jk)):
+      // long column runs over long probe lists.
+      static const char* bands_env = getenv("BBTC_BANDS");
+      static const bool bands = bands_env != nullptr;
+      static const bool band_cost = bands && std::string(bands_env) == "cost";
+      static const double band_ratio = getenv("BBTC_BAND_RATIO") ? atof(getenv("BBTC_BAND_RATIO")) : 4.0;
       static const double band_bytes = getenv("BBTC_BAND_BYTES") ? atof(getenv("BBTC_BAND_BYTES")) : 32e6;
       plan->band_shift.assign(nb, -1);
       for (uint32_t b = 0; b < nb; ++b) {
@@ -1400,11 +1407,25 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
         if (B.nnz == 0) continue;
         const int bits = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
         const uint32_t rows_i = plan->cuts[B.i + 1] - plan->cuts[B.i];
+        const uint32_t cols_j = plan->cuts[B.j + 1] - plan->cuts[B.j];
         int shift = -1;
         if (bands && rows_i > 1) {
           double probe = 0;   // the largest probe block this block's tasks gather from
-          for (uint32_t k = B.j; k < pe; ++k)
-            probe = std::max(probe, 4.0 * (double)plan->blocks[block_id(B.i, k)].nnz + 4.0 * rows_i);
+          double probe_words = 0, staged_words = 0;
+          for (uint32_t k = B.j; k < pe; ++k) {
+            const double nik = (double)plan->blocks[block_id(B.i, k)].nnz;
+            const double njk = (double)plan->blocks[block_id(B.j, k)].nnz;
+            probe = std::max(probe, 4.0 * nik + 4.0 * rows_i);
+            probe_words += (double)B.nnz * nik / rows_i;
+            staged_words += std::min<double>(cols_j, (double)B.nnz) * (cols_j ? njk / cols_j : 0.0);
+          }
+          const double nbands = std::ceil(probe / band_bytes);
+          if (tr.on)
+            fprintf(stderr, "[bbtc] band rule block (%u,%u): probe %.3g words, restaged %.3g words x %.0f bands%s\n",
+                    B.i, B.j, probe_words, staged_words, nbands,
+                    probe > band_bytes && (!band_cost || probe_words >= band_ratio * nbands * staged_words) ? " -> banded"
+                                                                                                        : "");
+          if (band_cost && probe_words < band_ratio * nbands * staged_words) probe = 0;
           if (probe > band_bytes) {
             const double band_rows = (double)rows_i * band_bytes / probe;
             shift = std::max(0, (int)std::floor(std::log2(std::max(1.0, band_rows))));

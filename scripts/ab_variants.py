@@ -2,6 +2,9 @@
 process builds the resident plan and reports median list / bit-row kernel ms of 5 counts.
 
     python scripts/ab_variants.py rmat24,orkut,friendster paper_2009_12457_b200/libbbtc.so build_ab/min6/libbbtc.so
+
+A variant may also be the default library under environment knobs: `env:K=V[;K2=V2]`
+(e.g. `env:BBTC_L2_FETCH=32`).
 """
 import json
 import os
@@ -22,7 +25,7 @@ del s, d
 plan = bb.Plan(ctx, g, p)
 ref = plan.count()[0]
 reps = [plan.count(timing=True)[2] for _ in range(5)]
-print(json.dumps({"config": name, "p": p, "lib": os.environ.get("BBTC_LIB", "default"), "triangles": ref,
+print(json.dumps({"config": name, "p": p, "lib": os.environ.get("BBTC_VARIANT", os.environ.get("BBTC_LIB", "default")), "triangles": ref,
                   "list_ms": statistics.median(r["t_kernel_ms"] - r["t_dense_ms"] for r in reps),
                   "dense_ms": statistics.median(r["t_dense_ms"] for r in reps),
                   "count_ms": statistics.median(r["t_kernel_ms"] for r in reps)}), flush=True)
@@ -33,7 +36,11 @@ libs = sys.argv[2:]
 for cfgp in configs:
     name, _, p = cfgp.partition(":")
     for lib in libs:
-        env = {**os.environ, "BBTC_LIB": os.path.abspath(lib)}
+        if lib.startswith("env:"):
+            kv = dict(x.split("=", 1) for x in lib[4:].split(";") if x)
+            env = {**os.environ, **kv, "BBTC_VARIANT": lib, "BBTC_LIB": os.path.abspath("paper_2009_12457_b200/libbbtc.so")}
+        else:
+            env = {**os.environ, "BBTC_LIB": os.path.abspath(lib)}
         r = subprocess.run([sys.executable, "-c", CHILD, name, p or "0"], env=env, capture_output=True, text=True,
                            timeout=1200)
         out = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
