@@ -31,6 +31,11 @@ static bool trace_enabled() {
   return on == 1;
 }
 
+bool sync_check() {
+  static const bool on = getenv("BBTC_SYNC_CHECK") != nullptr;
+  return on;
+}
+
 Trace::Trace(cudaStream_t s, const char* name) : st(s), phase(name), on(trace_enabled()) { mark("begin"); }
 
 void Trace::mark(const char* what) {

@@ -15,6 +15,8 @@
 // the list lengths, and needs no order inside the lists.
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "internal.h"
 
 namespace bbtc {
@@ -75,6 +77,28 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 #ifndef BBTC_P1_DEPTH
 #define BBTC_P1_DEPTH 4   // A/B: 8 = rounds of eight 32-word loads in flight for long probe lists
 #endif
+#ifndef BBTC_DEBUG_BOUNDS
+#define BBTC_DEBUG_BOUNDS 0   // debug builds: bounds checks in the list kernel (report via mapped host memory)
+#endif
+#if BBTC_DEBUG_BOUNDS
+// [0] = failing check id (first one wins), [1..7] = its values; [8] = m, [9] = row-offset words.
+__device__ unsigned long long* g_dbg;
+__device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long long a, unsigned long long b,
+                                      unsigned long long c, unsigned long long d, unsigned long long e,
+                                      unsigned long long f, unsigned long long g) {
+  if (atomicCAS(g_dbg, 0ull, code) == 0ull) {
+    g_dbg[1] = a; g_dbg[2] = b; g_dbg[3] = c; g_dbg[4] = d; g_dbg[5] = e; g_dbg[6] = f; g_dbg[7] = g;
+    __threadfence_system();
+  }
+  __trap();
+}
+#define DBG_CHECK(cond, code, a, b, c, d, e, f, g) \
+  do {                                             \
+    if (!(cond)) dbg_fail(code, a, b, c, d, e, f, g); \
+  } while (0)
+#else
+#define DBG_CHECK(cond, code, a, b, c, d, e, f, g) do { } while (0)
+#endif
 #ifndef BBTC_PF_NEXT
 #define BBTC_PF_NEXT 0   // A/B: rolling L2 prefetch of the next long probe list and of the remainders
 #endif
@@ -123,6 +147,7 @@ __device__ __forceinline__ void flatten(uint2* pay, int lane, bool nonempty, uin
     const uint32_t d = start - f0;
     const uint32_t starts = __reduce_or_sync(kFull, (nonempty && d < 32) ? (1u << d) : 0u);
     const uint32_t idx = before + __popc(starts & lanemask_le(lane)) - 1;
+    DBG_CHECK(f0 + lane >= total || idx < 32, 4, f0, idx, before, starts, total, start, 0);
     before += __popc(starts);
     return idx;
   };
@@ -147,37 +172,46 @@ __device__ __forceinline__ void flatten(uint2* pay, int lane, bool nonempty, uin
   __syncwarp();
 }
 
-// Buckets of kBW words (BBTC_BUCKET_WORDS; 4 by default: one LDS.128 per probe).  A
-// table is sized in 4-word units (nb4 of them) and addressed in buckets of kBW words.
+// Hash tables of buckets of BW words, linear probing over buckets; a table is sized in
+// 4-word units (nb4 of them) and addressed in buckets of BW words.  4-word buckets take
+// one LDS.128 per probe; 2-word buckets (LDS.64) measured faster in the bitmap kernel
+// variant (rmat24 list kernel 31.9 -> 31.2 ms, orkut 11.76 -> 11.47) and slower in the
+// hash-only one (friendster 333 -> 351 ms; 1-word buckets slower everywhere:
+// profiles/r02/r02m), so the width follows the variant (BBTC_BUCKET_WORDS[_BM]).
 #ifndef BBTC_BUCKET_WORDS
 #define BBTC_BUCKET_WORDS 4
 #endif
-constexpr int kBW = BBTC_BUCKET_WORDS;
-static_assert(kBW == 1 || kBW == 2 || kBW == 4, "bucket width");
+#ifndef BBTC_BUCKET_WORDS_BM
+#define BBTC_BUCKET_WORDS_BM 2
+#endif
 struct TabGeom {
   uint32_t bmask;
   int shift;
 };
+template <int BW>
 __device__ __forceinline__ TabGeom tab_geom(uint32_t nb4) {
-  const uint32_t nb = nb4 * (4 / kBW);
+  static_assert(BW == 1 || BW == 2 || BW == 4, "bucket width");
+  const uint32_t nb = nb4 * (4 / BW);
   return {nb - 1, 32 - (__ffs(nb) - 1)};
 }
 
-// Inserts key hk into the table (linear probing over buckets).
+// Inserts key hk into the table.
+template <int BW>
 __device__ __forceinline__ void table_insert(uint32_t* tab, uint32_t hk, TabGeom G) {
   uint32_t h = hbucket(hk, G.shift);
   for (;;) {
-    uint32_t* bk = tab + kBW * h;
+    uint32_t* bk = tab + BW * h;
 #pragma unroll
-    for (int x = 0; x < kBW; ++x)
+    for (int x = 0; x < BW; ++x)
       if (atomicCAS(bk + x, kEmpty, hk) == kEmpty) return;
     h = (h + 1) & G.bmask;
   }
 }
 
+template <int BW>
 __device__ __forceinline__ uint32_t table_probe(const uint32_t* tab, uint32_t hk, TabGeom G) {
   uint32_t h = hbucket(hk, G.shift);
-  if constexpr (kBW == 4) {
+  if constexpr (BW == 4) {
     const uint4* tab4 = reinterpret_cast<const uint4*>(tab);
     uint4 q = tab4[h];
     bool hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
@@ -187,7 +221,7 @@ __device__ __forceinline__ uint32_t table_probe(const uint32_t* tab, uint32_t hk
       hit = (q.x == hk) | (q.y == hk) | (q.z == hk) | (q.w == hk);
     }
     return hit;
-  } else if constexpr (kBW == 2) {
+  } else if constexpr (BW == 2) {
     const uint2* tab2 = reinterpret_cast<const uint2*>(tab);
     uint2 q = tab2[h];
     bool hit = (q.x == hk) | (q.y == hk);
@@ -215,6 +249,9 @@ template <class Test>
 __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ cols, uint2* pay, int lane, uint32_t bx,
                                                 uint32_t bl, uint32_t slot, Test test) {
   uint32_t hits = 0;
+#if BBTC_DEBUG_BOUNDS
+  DBG_CHECK((unsigned long long)bx + bl <= g_dbg[8], 3, bx, bl, slot, g_dbg[8], 0, 0, 0);
+#endif
   uint32_t longs = __ballot_sync(kFull, bl >= 32);
 #if BBTC_PF_NEXT
   // Rolling L2 prefetch: every lane asks for its own < 32-word remainder now (phase 2
@@ -311,13 +348,13 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
     const uint32_t cn = min((uint32_t)kChunk, total_a - c0);
     uint32_t nb = 16;
     while (2 * nb < cn) nb <<= 1;
-    const TabGeom G = tab_geom(nb);
+    const TabGeom G = tab_geom<4>(nb);
     for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncwarp();
-    for (uint32_t x = lane; x < cn; x += 32) table_insert(tab, ld_stream(cS + s0 + c0 + x), G);
+    for (uint32_t x = lane; x < cn; x += 32) table_insert<4>(tab, ld_stream(cS + s0 + c0 + x), G);
     __syncwarp();
     hits += probe_lists(cols, pay, lane, bx, bl, 0,
-                        [&](uint32_t w, uint32_t) { return table_probe(tab, w, G); });
+                        [&](uint32_t w, uint32_t) { return table_probe<4>(tab, w, G); });
   }
   return hits;
 }
@@ -419,7 +456,10 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       uint32_t mid = (lo + hi + 1) >> 1;
       if (item_start[mid] <= g) lo = mid; else hi = mid - 1;
     }
+    DBG_CHECK(lo < n_exec, 6, lo, n_exec, g, 0, 0, 0, 0);
     const TaskDesc T = tasks[lo];
+    DBG_CHECK(T.ij < g_dbg[10] && T.ik < g_dbg[10] && T.jk < g_dbg[10] && T.idx < n_tasks, 7, T.ij, T.ik, T.jk, T.idx,
+              g_dbg[10], n_tasks, 0);
     if (ready) {
       // Streaming (a6): wait until the copy engine has delivered the task's blocks.
       if (lane == 0) {
@@ -465,12 +505,18 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
       uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;   // a: staged list, b: probe list
+      DBG_CHECK(!valid || ((!kCol || key < Bij.nc) && BS.ro + key + 1 < g_dbg[9] && BP.ro + pid + 1 < g_dbg[9]), 5,
+                T.idx, e, u, v, BS.ro, BP.ro, Bij.nc);
       if (valid) {
         a0 = rpS[key];
         alen = rpS[key + 1] - a0;
         b0 = rpP[pid];
         blen = rpP[pid + 1] - b0;
       }
+      DBG_CHECK(!valid || ((!kCol || v < Bij.nc) && a0 + alen <= BS.nnz && b0 + blen <= BP.nnz && alen <= BS.nnz &&
+                           blen <= BP.nnz && e < Bij.e0 + Bij.nnz),
+                1, T.idx, e, u, v, ((unsigned long long)a0 << 32) | alen, ((unsigned long long)b0 << 32) | blen,
+                ((unsigned long long)BS.nnz << 32) | BP.nnz);
       const uint32_t kprev = __shfl_up_sync(kFull, key, 1);
       const bool leader = valid && (lane == 0 || key != kprev);
       const uint32_t lmask = __ballot_sync(kFull, leader);
@@ -589,13 +635,22 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           if (lmask == 1u) {   // one list: coalesced reads, no flattening
             const uint32_t s0 = __shfl_sync(kFull, a0, 0), sn = __shfl_sync(kFull, alen, 0);
             for (uint32_t x = lane; x < sn; x += 32) {
+              DBG_CHECK(s0 + x < BS.nnz, 8, s0, x, BS.nnz, T.idx, 0, 0, 0);
               const uint32_t w = ld_stream(cS + s0 + x);
+              DBG_CHECK((w >> 5) < bmw, 9, w, bmw, T.idx, 0, 0, 0, 0);
               atomicOr(bm + (w >> 5), 1u << (w & 31));
             }
           } else {
             flatten(pay, lane, leader && alen > 0, aoff, make_uint2(a0 - aoff, slot * bmw),
-                    __shfl_sync(kFull, aend, L - 1), [&](uint32_t f, uint2 P) { return ld_stream(cS + P.x + f); },
-                    [&](uint32_t, uint2 P, uint32_t w) { atomicOr(bm + P.y + (w >> 5), 1u << (w & 31)); });
+                    __shfl_sync(kFull, aend, L - 1),
+                    [&](uint32_t f, uint2 P) {
+                      DBG_CHECK(P.x + f < BS.nnz, 10, P.x, f, BS.nnz, T.idx, 0, 0, 0);
+                      return ld_stream(cS + P.x + f);
+                    },
+                    [&](uint32_t, uint2 P, uint32_t w) {
+                      DBG_CHECK(P.y + (w >> 5) < (uint32_t)kTable && (w >> 5) < bmw, 11, P.y, w, bmw, T.idx, 0, 0, 0);
+                      atomicOr(bm + P.y + (w >> 5), 1u << (w & 31));
+                    });
           }
           __syncwarp();
           auto test = [bm](uint32_t w, uint32_t base_w) { return (bm[base_w + (w >> 5)] >> (w & 31)) & 1u; };
@@ -609,14 +664,19 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           const uint32_t total_a = __shfl_sync(kFull, aend, L - 1);
           uint32_t nb = 16;
           while ((dense || kLoadHalf ? 2 * nb : nb) < total_a) nb <<= 1;
-          const TabGeom G = tab_geom(nb);
+          constexpr int BW = kBm ? BBTC_BUCKET_WORDS_BM : BBTC_BUCKET_WORDS;
+          const TabGeom G = tab_geom<BW>(nb);
+          DBG_CHECK(nb <= kTable / 4, 2, T.idx, nb, total_a, L, dense, longl, 0);
           for (uint32_t x = lane; x < nb; x += 32) tab4[x] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncwarp();
           flatten(pay, lane, in && leader && alen > 0, aoff, make_uint2(a0 - aoff, slot), total_a,
-                  [&](uint32_t f, uint2 P) { return ld_stream(cS + P.x + f); },
-                  [&](uint32_t, uint2 P, uint32_t w) { table_insert(tab, (w << 5) | P.y, G); });
+                  [&](uint32_t f, uint2 P) {
+                    DBG_CHECK(P.x + f < BS.nnz, 12, P.x, f, BS.nnz, T.idx, 0, 0, 0);
+                    return ld_stream(cS + P.x + f);
+                  },
+                  [&](uint32_t, uint2 P, uint32_t w) { table_insert<BW>(tab, (w << 5) | P.y, G); });
           // ---- probe every word of each lane's list P against its staged list
-          auto test = [&](uint32_t w, uint32_t sl) { return table_probe(tab, (w << 5) | sl, G); };
+          auto test = [&](uint32_t w, uint32_t sl) { return table_probe<BW>(tab, (w << 5) | sl, G); };
           hits += probe_lists(cols, pay, lane, bx, bl, slot, test);
           continue_run(test);
         }
@@ -897,11 +957,33 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
     own.blocks = plan->d_blocks.p;
     ar = &own;
   }
+#if BBTC_DEBUG_BOUNDS
+  static unsigned long long* h_dbg = nullptr;
+  if (!h_dbg) {
+    BBTC_CUDA(cudaHostAlloc((void**)&h_dbg, 16 * 8, cudaHostAllocMapped));
+    unsigned long long* d_dbg = nullptr;
+    BBTC_CUDA(cudaHostGetDevicePointer((void**)&d_dbg, h_dbg, 0));
+    BBTC_CUDA(cudaMemcpyToSymbol(g_dbg, &d_dbg, sizeof d_dbg));
+  }
+  BBTC_CUDA(cudaStreamSynchronize(st));
+  std::memset(h_dbg, 0, 16 * 8);
+  h_dbg[8] = ar != &own ? ~0ull : plan->m;   // (window arenas: no bound known here)
+  uint64_t ro_words = 0;
+  for (auto& B : plan->blocks) ro_words += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
+  h_dbg[9] = ar != &own ? ~0ull : ro_words;
+  h_dbg[10] = plan->blocks.size();
+#endif
   kern<<<(unsigned)grid, kWarps * 32, kSmemBytes, st>>>(
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
       n_exec ? n_exec : (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
       (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col, (unsigned long long*)ctx->task_cycles);
+#if BBTC_DEBUG_BOUNDS
+  cudaStreamSynchronize(st);
+  if (h_dbg[0])
+    fprintf(stderr, "[bbtc debug] k_count check %llu failed: %llu %llu %llu %llu %llu %llu %llu (m %llu, ro %llu)\n",
+            h_dbg[0], h_dbg[1], h_dbg[2], h_dbg[3], h_dbg[4], h_dbg[5], h_dbg[6], h_dbg[7], h_dbg[8], h_dbg[9]);
+#endif
   BBTC_LAUNCHED(ctx);
 }
 

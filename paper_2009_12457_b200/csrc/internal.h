@@ -27,9 +27,11 @@ struct Error {
   } while (0)
 #define BBTC_STR2_(x) #x
 #define BBTC_STR_(x) BBTC_STR2_(x)
+bool sync_check();   // BBTC_SYNC_CHECK=1: every launch is followed by a device sync (fault location)
 #define BBTC_LAUNCHED(ctx)                                                                     \
   do {                                                                                         \
-    cudaError_t e_ = cudaGetLastError();                                                       \
+    cudaError_t e_ = ::bbtc::sync_check() ? cudaDeviceSynchronize() : cudaSuccess;             \
+    if (e_ == cudaSuccess) e_ = cudaGetLastError();                                            \
     if (e_ != cudaSuccess)                                                                     \
       ::bbtc::raise(BBTC_ECUDA, std::string("kernel launched at " __FILE__ ":" BBTC_STR_(__LINE__) ": ") + \
                                     cudaGetErrorString(e_));                                   \

@@ -41,12 +41,58 @@ void cub_call(bbtc_ctx* ctx, F f, uint64_t kernels = 2) {
   DevBuf<uint8_t> tmp;
   tmp.alloc(std::max<size_t>(bytes, 1), ctx);
   BBTC_CUDA(f((void*)tmp.p, bytes));
+  if (sync_check()) BBTC_CUDA(cudaDeviceSynchronize());
   ctx->launches += kernels;
 }
 
 // Onesweep radix sort: histogram + exclusive-sum kernels, then one pass per 8-bit
 // digit for every portion of up to 2^28 items.
 inline uint64_t radix_kernels(uint64_t n, int bits) { return 2 + (uint64_t)((bits + 7) / 8) * (n / (1ull << 28) + 1); }
+
+// 64-bit-key onesweep with a B200 tile: CUB's sm_100 policy for 8-byte keys is 384
+// threads x 30 keys per CTA; smaller CTAs measured faster on this B200 for every
+// 64-bit-key sort of the path (scripts/micro/sorttune.cu, profiles/r02/sorttune/: 268 M
+// keys, 48 bits 16.2 -> 10.9 ms at 288 x 32; 260 M keys, 28 bits 11.0 -> 8.0 ms at
+// 256 x 30).  Only the onesweep policy
+// differs from CUB's own hub; u32 key-value sorts keep CUB's tuning (measured best).
+template <class K, class V, int kT, int kI>
+struct OnesweepHub {
+  using Base = typename cub::detail::radix::policy_hub<K, V, unsigned long long>::Policy1000;
+  struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
+    static constexpr bool ONESWEEP = true;
+    static constexpr int ONESWEEP_RADIX_BITS = 8;
+    using HistogramPolicy = typename Base::HistogramPolicy;
+    using ExclusiveSumPolicy = typename Base::ExclusiveSumPolicy;
+    using OnesweepPolicy =
+        cub::AgentRadixSortOnesweepPolicy<kT, kI, K, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT, 8>;
+    using ScanPolicy = typename Base::ScanPolicy;
+    using DownsweepPolicy = typename Base::DownsweepPolicy;
+    using AltDownsweepPolicy = typename Base::AltDownsweepPolicy;
+    using UpsweepPolicy = typename Base::UpsweepPolicy;
+    using AltUpsweepPolicy = typename Base::AltUpsweepPolicy;
+    using SingleTilePolicy = typename Base::SingleTilePolicy;
+    using SegmentedPolicy = typename Base::SegmentedPolicy;
+    using AltSegmentedPolicy = typename Base::AltSegmentedPolicy;
+  };
+  using MaxPolicy = Policy1000;
+};
+// Keys-only sort of 64-bit keys over bits [b0, b1), DoubleBuffer semantics (the sorted
+// keys end in keys.Current()), same contract as cub::DeviceRadixSort::SortKeys.
+inline cudaError_t sort_keys64(void* tmp, size_t& bytes, cub::DoubleBuffer<uint64_t>& keys, uint64_t n, int b0,
+                               int b1, cudaStream_t st) {
+  static const bool stock = getenv("BBTC_CUB_STOCK") != nullptr;   // A/B: CUB's own tuning
+  cub::DoubleBuffer<cub::NullType> none;
+  if (stock) return cub::DeviceRadixSort::SortKeys(tmp, bytes, keys, n, b0, b1, st);
+  // > 4 digits (the 48-bit canonical keys): 288 x 32 (10.9 ms vs 12.0 at 256 x 30);
+  // <= 4 digits (block keys): 256 x 30 (8.0 ms; 256 x 40 equal).
+  using Wide = cub::DispatchRadixSort<false, uint64_t, cub::NullType, unsigned long long,
+                                      OnesweepHub<uint64_t, cub::NullType, 288, 32>>;
+  using Narrow = cub::DispatchRadixSort<false, uint64_t, cub::NullType, unsigned long long,
+                                        OnesweepHub<uint64_t, cub::NullType, 256, 30>>;
+  if (b1 - b0 > 32) return Wide::Dispatch(tmp, bytes, keys, none, (unsigned long long)n, b0, b1, true, st);
+  return Narrow::Dispatch(tmp, bytes, keys, none, (unsigned long long)n, b0, b1, true, st);
+}
 
 // ---- a1 ------------------------------------------------------------------------------
 // key = (min << bw) | max for a != b, kSentinel for self-loops; tracks the largest id.
@@ -892,13 +938,13 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   if (stream_sort) {
     alt.alloc(E, ctx);
     cub::DoubleBuffer<uint64_t> db0(keys.p, alt.p);
-    BBTC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_tmp_bytes, db0, piece, 0, 2 * bw, ctx->aux_stream));
+    BBTC_CUDA(sort_keys64(nullptr, sort_tmp_bytes, db0, piece, 0, 2 * bw, ctx->aux_stream));
     sort_tmp.alloc(std::max<size_t>(sort_tmp_bytes, 1), ctx);
   }
   auto sort_piece = [&](uint64_t off, uint64_t len, int width) {
     cub::DoubleBuffer<uint64_t> db(keys.p + off, alt.p + off);
     size_t tb = sort_tmp_bytes;
-    BBTC_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, db, len, 0, 2 * width, ctx->aux_stream));
+    BBTC_CUDA(sort_keys64(sort_tmp.p, tb, db, len, 0, 2 * width, ctx->aux_stream));
     ctx->launches += radix_kernels(len, 2 * width);
     pieces.push_back({off, len, db.selector});
   };
@@ -1034,7 +1080,7 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       if (!alt.p) alt.alloc(E, ctx);
       cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
       cub_call(ctx, [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, db, E, 0, bw + bid, st);
+        return sort_keys64(t, b, db, E, 0, bw + bid, st);
       }, radix_kernels(E, bw + bid));
       in_keys = db.Current() == keys.p;
     }
@@ -1249,7 +1295,7 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     cub_call(ctx, [&](void* t, size_t& b) {
       // Only the (j, ru) bits: the count kernel hashes lists, so the columns of a row
       // need no order (sorting them too would cost 3 more radix passes).
-      return cub::DeviceRadixSort::SortKeys(t, b, db, m, getenv("BBTC_SORT_ROWS") ? 0 : bn, bp + 2 * bn, st);
+      return sort_keys64(t, b, db, m, getenv("BBTC_SORT_ROWS") ? 0 : bn, bp + 2 * bn, st);
     }, radix_kernels(m, bp + bn));
     if (db.Current() != ck.p) std::swap(ck, ck_alt);
     ck_alt.reset();
@@ -1685,7 +1731,7 @@ static uint64_t sort_unique(bbtc_ctx* ctx, DevBuf<uint64_t>& keys, uint64_t cnt,
   DevBuf<uint64_t> alt;
   alt.alloc(cnt, ctx);
   cub::DoubleBuffer<uint64_t> db(keys.p, alt.p);
-  cub_call(ctx, [&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, 2 * bw, st); },
+  cub_call(ctx, [&](void* t, size_t& b) { return sort_keys64(t, b, db, cnt, 0, 2 * bw, st); },
            radix_kernels(cnt, 2 * bw));
   if (db.Current() != keys.p) std::swap(keys, alt);
   DevBuf<uint64_t> nsel;

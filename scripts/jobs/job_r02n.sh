@@ -1,0 +1,7 @@
+#!/bin/bash
+# Bands crash with a bounds-checking build; CUB onesweep tunings.
+out=gpurun_out/${OUT:-r02n}; mkdir -p $out
+BBTC_LIB=$PWD/build_ab/dbg/libbbtc.so BBTC_BANDS=1 BBTC_BAND_BYTES=65536 CUDA_LAUNCH_BLOCKING=1 timeout 300 python tests/gpu_child.py rmat:16:16:9 4 resident > $out/bands_dbg.log 2>&1; echo "bands rc=$?" >> $out/steps.txt
+BBTC_LIB=$PWD/build_ab/dbg/libbbtc.so CUDA_LAUNCH_BLOCKING=1 timeout 300 python tests/gpu_child.py rmat:16:16:9 4 resident > $out/nobands_dbg.log 2>&1; echo "nobands rc=$?" >> $out/steps.txt
+timeout 600 scripts/micro/sorttune > $out/sorttune.log 2>&1; echo "sorttune rc=$?" >> $out/steps.txt
+echo done >> $out/steps.txt

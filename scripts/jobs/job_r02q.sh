@@ -1,0 +1,7 @@
+#!/bin/bash
+out=gpurun_out/${OUT:-r02q}; mkdir -p $out
+BBTC_SYNC_CHECK=1 BBTC_LIB=$PWD/build_ab/dbg/libbbtc.so BBTC_BANDS=1 BBTC_BAND_BYTES=65536 timeout 300 python tests/gpu_child.py rmat:16:16:9 4 resident > $out/bands_dbg.log 2>&1; echo "bands rc=$?" >> $out/steps.txt
+BBTC_SYNC_CHECK=1 BBTC_BANDS=1 BBTC_BAND_BYTES=65536 timeout 300 python tests/gpu_child.py rmat:16:16:9 4 resident > $out/bands_head.log 2>&1; echo "bands head rc=$?" >> $out/steps.txt
+BBTC_SYNC_CHECK=1 BBTC_BANDS=1 BBTC_BAND_BYTES=1000000 timeout 300 python tests/gpu_child.py rmat:16:16:9 4 resident > $out/bands_1m.log 2>&1; echo "bands 1m rc=$?" >> $out/steps.txt
+timeout 900 scripts/micro/sorttune > $out/sorttune.log 2>&1; echo "sorttune rc=$?" >> $out/steps.txt
+echo done >> $out/steps.txt
