@@ -626,7 +626,8 @@ def main():
                          "count_out_of_core_half_budget": tm_o["t_total_ms"], "h2d_bytes_out_of_core": tm_o["h2d_bytes"],
                          "gen_s": t_gen},
         "plan": {"lambda": pinfo["lambda"], "dmax_blk": pinfo["dmax_blk"], "visits": pinfo["visits"],
-                 "b_alg": pinfo["b_alg"], "work_items": pinfo["work_items"], "block_bytes": pinfo["block_bytes"]},
+                 "b_alg": pinfo["b_alg"], "work_items": pinfo["work_items"], "block_bytes": pinfo["block_bytes"],
+                 "slot_bytes": pinfo.get("slot_bytes", 0)},
         "paper_context": "BBTC on 8xV100 DGX-1 hybrid, copy incl.: R-MAT scale24 1.154 s = 2.3e8 edges/s "
                          "(P:1182-1186); Friendster 3.133 s = 5.8e8 edges/s (P:1200-1204). Other hardware.",
     }

@@ -183,6 +183,9 @@ typedef struct {
   uint64_t dense_edge_bytes;/* compulsory reads of the bit-row kernel besides the bit rows
                                (dense_bytes): the per-edge iteration arrays of the distinct G_ij
                                blocks the dense tasks walk */
+  uint64_t slot_bytes;      /* device bytes of the probe slots (8 words per row of each probe
+                               block with many short rows: length, CSR offset, first 6 ids),
+                               read by resident counts instead of the row offsets; 0 = none */
 } bbtc_plan_info;
 
 #define BBTC_PLAN_STATS 1u     /* compute b_alg / visits / dmax_blk (one extra device pass) */

@@ -56,7 +56,7 @@ class bbtc_plan_info(ctypes.Structure):
                 ("block_bytes", c_u64), ("max_task_bytes", c_u64), ("b_alg", c_u64), ("visits", c_u64),
                 ("work_items", c_u64), ("sum_a", c_u64), ("sum_b", c_u64),
                 ("dense_tasks", c_u32), ("dense_bits", c_u32), ("dense_bytes", c_u64), ("stream_bytes", c_u64),
-                ("list_read_bytes", c_u64), ("dense_edge_bytes", c_u64)]
+                ("list_read_bytes", c_u64), ("dense_edge_bytes", c_u64), ("slot_bytes", c_u64)]
 
 
 class bbtc_edge_list(ctypes.Structure):

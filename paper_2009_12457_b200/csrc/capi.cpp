@@ -870,6 +870,7 @@ BBTC_API bbtc_status bbtc_plan_to_host(bbtc_ctx* ctx, bbtc_plan* plan) {
     }
     BBTC_CUDA(cudaStreamSynchronize(st));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
+    plan->slots_ready = false;   // (the slots live in the cols arena)
     if (plan->colmajor) plan->rows.reset();   // (kept only for the dense row walk of resident plans)
     plan->rowptr.reset();
     plan->dense.reset();
@@ -931,6 +932,7 @@ BBTC_API bbtc_status bbtc_unstage(bbtc_ctx* ctx, bbtc_plan* plan) {
     if (!plan->host_blocks) return;   // device plans own their only copy
     BBTC_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& A : plan->edge_arenas()) A.dev->reset();
+    plan->slots_ready = false;   // (the slots live in the cols arena)
     plan->rowptr.reset();
     plan->d_colptr.reset();
     plan->dense.reset();

@@ -119,9 +119,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
   return x;
 }
 
-// Length of the run of set bits from lane 0.  Equal staged keys are contiguous in a
-// column-ordered block, but not in a row-banded one (a column reappears in the next
-// band): a batch or run takes only the leading lanes of its key.
+// Length of the run of set bits from lane 0: a batch or run takes only the leading
+// lanes of its key (equal keys are contiguous in a column-ordered block; the prefix
+// rule keeps the kernel correct for any walk order).
 __device__ __forceinline__ int lane_prefix(uint32_t b) { return b == kFull ? 32 : __ffs(~b) - 1; }
 
 __device__ __forceinline__ uint32_t lanemask_le(int lane) { return 0xffffffffu >> (31 - lane); }
@@ -429,7 +429,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         uint32_t rank, uint32_t world, unsigned long long* __restrict__ cursor,
         unsigned long long* __restrict__ counts, uint32_t n_tasks, const uint32_t* ready, uint32_t epoch,
         const uint32_t* __restrict__ colptr, const uint32_t* __restrict__ item_col,
-        unsigned long long* __restrict__ task_cycles) {
+        unsigned long long* __restrict__ task_cycles, const uint32_t* __restrict__ slot_of) {
   static_assert(!kCP || kCol, "column offsets replace the column ids of a column-major walk");
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -486,6 +486,21 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
     const uint32_t* rpS = rowptr + BS.ro;
     const uint32_t* cS = cols + BS.e0;
     const uint32_t* rpP = rowptr + BP.ro;
+    // Probe slots (resident plans): the probe block's row r at cols[so + 8r] = {len,
+    // CSR offset, first 6 ids}; rows of <= 6 entries are probed in the slot itself.
+    const uint32_t so = slot_of ? slot_of[kCol ? T.ik : T.jk] : 0u;
+    // probe list of row r of the probe block: its index in the cols arena and length
+    auto probe_of = [&](uint32_t r, uint32_t& x, uint32_t& len) {
+      if (so) {
+        const uint2 h = *reinterpret_cast<const uint2*>(cols + so + 8 * r);
+        len = h.x;
+        x = h.x <= 6 ? so + 8 * r + 2 : (uint32_t)BP.e0 + h.y;
+      } else {
+        const uint32_t b0 = rpP[r];
+        len = rpP[r + 1] - b0;
+        x = (uint32_t)BP.e0 + b0;
+      }
+    };
     // kCP: G_ij's column offsets, unless the block ships its column ids (kNoColptr)
     const bool cpm = kCP && Bij.co != kNoColptr;
     const uint32_t* cpb = cpm ? colptr + Bij.co : nullptr;
@@ -504,18 +519,17 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       else v = valid ? ld_stream(it_v + e) : 0xFFFFFFFFu;
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
-      uint32_t a0 = 0, alen = 0, b0 = 0, blen = 0;   // a: staged list, b: probe list
+      uint32_t a0 = 0, alen = 0, bx = 0, blen = 0;   // a: staged list, b: probe list (bx: index in cols)
       DBG_CHECK(!valid || ((!kCol || key < Bij.nc) && BS.ro + key + 1 < g_dbg[9] && BP.ro + pid + 1 < g_dbg[9]), 5,
                 T.idx, e, u, v, BS.ro, BP.ro, Bij.nc);
       if (valid) {
         a0 = rpS[key];
         alen = rpS[key + 1] - a0;
-        b0 = rpP[pid];
-        blen = rpP[pid + 1] - b0;
+        probe_of(pid, bx, blen);
       }
-      DBG_CHECK(!valid || ((!kCol || v < Bij.nc) && a0 + alen <= BS.nnz && b0 + blen <= BP.nnz && alen <= BS.nnz &&
-                           blen <= BP.nnz && e < Bij.e0 + Bij.nnz),
-                1, T.idx, e, u, v, ((unsigned long long)a0 << 32) | alen, ((unsigned long long)b0 << 32) | blen,
+      DBG_CHECK(!valid || ((!kCol || v < Bij.nc) && a0 + alen <= BS.nnz && blen <= BP.nnz && alen <= BS.nnz &&
+                           e < Bij.e0 + Bij.nnz),
+                1, T.idx, e, u, v, ((unsigned long long)a0 << 32) | alen, ((unsigned long long)bx << 32) | blen,
                 ((unsigned long long)BS.nnz << 32) | BP.nnz);
       const uint32_t kprev = __shfl_up_sync(kFull, key, 1);
       const bool leader = valid && (lane == 0 || key != kprev);
@@ -546,7 +560,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
       const bool in = lane < L;
       // edges whose staged list is empty cannot close a triangle: no probes for them
       const uint32_t bl = (in && alen > 0) ? blen : 0;
-      const uint32_t bx = (uint32_t)BP.e0 + b0;   // index of P[0] in the cols arena
       // Ask L2 for every lane's probe list now (fire-and-forget, no registers): the
       // 32 random gathers of the batch then overlap the staging of S instead of each
       // list's first round waiting out a full DRAM latency in turn.
@@ -579,30 +592,24 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
             uint32_t p_cur, p_nxt;
             bool ok_cur = edge(e2, p_cur);
             bool ok_nxt = edge(e2 + 32, p_nxt);
-            uint32_t b2 = 0, bl2 = 0;
-            if (ok_cur && alen > 0) {
-              b2 = rpP[p_cur];
-              bl2 = rpP[p_cur + 1] - b2;
-            }
+            uint32_t x2 = 0, bl2 = 0;
+            if (ok_cur && alen > 0) probe_of(p_cur, x2, bl2);
             for (;;) {
               const int L2 = lane_prefix(__ballot_sync(kFull, ok_cur));   // the run's edges
               if (L2 == 0) break;
-              uint32_t bn = 0, bln = 0, p_nn = 0;
+              uint32_t xn = 0, bln = 0, p_nn = 0;
               bool ok_nn = false;
               if (L2 == 32) {
-                if (ok_nxt && alen > 0) {
-                  bn = rpP[p_nxt];
-                  bln = rpP[p_nxt + 1];
-                }
+                if (ok_nxt && alen > 0) probe_of(p_nxt, xn, bln);
                 ok_nn = edge(e2 + 64, p_nn);
               }
-              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, lane < L2 ? bl2 : 0u, 0, test);
+              hits += probe_lists(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
               e2 += 32;
               ok_cur = ok_nxt;
-              b2 = bn;
-              bl2 = bln - bn;
+              x2 = xn;
+              bl2 = bln;
               ok_nxt = ok_nn;
               p_nxt = p_nn;
             }
@@ -612,13 +619,9 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
               const bool ok = e2 < e_end && same(e2);
               const int L2 = lane_prefix(__ballot_sync(kFull, ok));   // the run's edges
               if (L2 == 0) break;
-              uint32_t b2 = 0, bl2 = 0;
-              if (ok && alen > 0) {
-                const uint32_t p2 = kCol ? it_u[e2] : it_v[e2];
-                b2 = rpP[p2];
-                bl2 = rpP[p2 + 1] - b2;
-              }
-              hits += probe_lists(cols, pay, lane, (uint32_t)BP.e0 + b2, lane < L2 ? bl2 : 0u, 0, test);
+              uint32_t x2 = 0, bl2 = 0;
+              if (ok && alen > 0) probe_of(kCol ? it_u[e2] : it_v[e2], x2, bl2);
+              hits += probe_lists(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
           }
@@ -912,7 +915,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   using KernT = void (*)(const uint32_t*, const uint32_t*, const uint32_t*, const uint32_t*, const BlockDesc*,
                          const TaskDesc*, const uint64_t*, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t,
                          unsigned long long*, unsigned long long*, uint32_t, const uint32_t*, uint32_t,
-                         const uint32_t*, const uint32_t*, unsigned long long*);
+                         const uint32_t*, const uint32_t*, unsigned long long*, const uint32_t*);
   // The bitmap variant only where some task's V_k is small enough (it costs the main
   // loop a few registers: friendster, whose parts are all large, measured 0.7% slower).
   bool bm = false;
@@ -949,6 +952,8 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   const int per = std::max(1, std::min(per_sm[variant], cap_env > 0 ? cap_env : kCtasPerSm));
   const uint64_t grid = std::min<uint64_t>((uint64_t)ctx->sm_count * per, (my_items + kWarps - 1) / kWarps);
   DevArenas own;
+  // probe slots only over the plan's own resident arenas (they live in its cols arena)
+  const uint32_t* slot_of = !ar && plan->slots_ready && !getenv("BBTC_NO_SLOTS_KERNEL") ? plan->d_slot_of.p : nullptr;
   if (!ar) {   // the plan's own (fully resident) arenas
     own.cols = plan->cols.p;
     own.it_u = plan->colmajor ? plan->ccu.p : plan->rows.p;
@@ -967,7 +972,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
   }
   BBTC_CUDA(cudaStreamSynchronize(st));
   std::memset(h_dbg, 0, 16 * 8);
-  h_dbg[8] = ar != &own ? ~0ull : plan->m;   // (window arenas: no bound known here)
+  h_dbg[8] = ar != &own || slot_of ? ~0ull : plan->m;   // (window arenas, slots: no bound known here)
   uint64_t ro_words = 0;
   for (auto& B : plan->blocks) ro_words += (uint64_t)(plan->cuts[B.i + 1] - plan->cuts[B.i]) + 1;
   h_dbg[9] = ar != &own ? ~0ull : ro_words;
@@ -977,7 +982,7 @@ void count_launch(bbtc_ctx* ctx, const bbtc_plan* plan, uint32_t rank, uint32_t 
       ar->cols, ar->it_u, ar->it_v, ar->rowptr, ar->blocks, tasks ? tasks : plan->d_tasks.p,
       item_start ? item_start : plan->d_item_start.p,
       n_exec ? n_exec : (uint32_t)plan->tasks.size(), item_lo, item_hi, rank, world, cursor, (unsigned long long*)d_counts,
-      (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col, (unsigned long long*)ctx->task_cycles);
+      (uint32_t)nt, ready, epoch, ar->colptr, ar->item_col, (unsigned long long*)ctx->task_cycles, slot_of);
 #if BBTC_DEBUG_BOUNDS
   cudaStreamSynchronize(st);
   if (h_dbg[0])

@@ -172,6 +172,11 @@ struct bbtc_plan {
   bbtc::DevBuf<uint32_t> rows;        // m: local row id u - cuts[i]
   bbtc::DevBuf<uint32_t> rowptr;      // sum over blocks of |V_i|+1
   bbtc::DevBuf<uint32_t> ccu, ccv;    // m: column-major iteration order (u, v) of each block
+  // probe slots (resident counts): per block the index in the cols arena of its |V_i|
+  // 8-word row slots (0 = none); valid while slots_ready (the arena was built with them)
+  std::vector<uint32_t> slot_of;
+  bbtc::DevBuf<uint32_t> d_slot_of;
+  bool slots_ready = false;
   bbtc::DevBuf<uint32_t> d_colptr;    // streamed column-major plans: per block at co, |V_j|+1 local column offsets
   bbtc::DevBuf<uint32_t> d_item_col;  // host plans: the column of every work item's first edge (at TaskDesc.icol)
   bool colmajor = true;               // kernel walks G_ij by column (ccu/ccv) vs by row (rows/cols)
@@ -196,7 +201,6 @@ struct bbtc_plan {
   // so nothing the persistent count kernel waits for needs an SM).
   uint32_t* h_colptr = nullptr;       // pinned, per block at co_off[b]: local edge offsets of its columns
   std::vector<uint64_t> rp_zero;      // per block: leading zero entries of its row offsets
-  std::vector<int> band_shift;        // per block: walk by (row >> shift, column) bands, -1 = plain columns
   std::vector<uint64_t> co_off;       // per block: first entry in the column-offset arena
   bool resident = true;               // device arenas hold every block
   bbtc_ctx* ctx = nullptr;

@@ -567,18 +567,24 @@ __global__ void k_block_first(const uint32_t* __restrict__ rowptr, const uint64_
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) starts[b] = rowptr[ro[b]];
 }
 
-// ---- a4 row bands (BBTC_BANDS, §7 "Row bands") --------------------------------------
-// key = (row >> shift) << cb | column: a block's column-major walk, split into bands of
-// 2^shift rows, so the probe lists a band gathers (rows of G_ik) stay L2-resident.
-__global__ void k_band_keys(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ cols, uint64_t n,
-                            int shift, int cb, uint32_t* __restrict__ keys) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
-    keys[e] = ((rows[e] >> shift) << cb) | cols[e];
-}
-__global__ void k_band_cols(uint32_t* __restrict__ keys, uint64_t n, int cb) {
-  const uint32_t mask = (1u << cb) - 1;
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x)
-    keys[e] &= mask;
+// ---- a4 probe slots: per row of a slot block, 8 words at cols[so + 8r]: the row's
+// length, its block-local CSR offset and its first min(len, 6) column ids.
+__global__ void k_slots(const uint32_t* __restrict__ rowptr, uint32_t* __restrict__ cols,
+                        const BlockDesc* __restrict__ blocks, const uint32_t* __restrict__ ids,
+                        const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ nrows) {
+  const uint32_t b = ids[blockIdx.y];
+  const BlockDesc B = blocks[b];
+  const uint32_t rows = nrows[b];
+  uint4* S = reinterpret_cast<uint4*>(cols + slot_of[b]);
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const uint32_t lo = rowptr[B.ro + r], len = rowptr[B.ro + r + 1] - lo;
+    const uint32_t* c = cols + B.e0 + lo;
+    uint32_t w[6];
+#pragma unroll
+    for (int x = 0; x < 6; ++x) w[x] = x < (int)len ? c[x] : 0u;
+    S[2 * (uint64_t)r] = make_uint4(len, lo, w[0], w[1]);
+    S[2 * (uint64_t)r + 1] = make_uint4(w[2], w[3], w[4], w[5]);
+  }
 }
 
 // ---- a4 transpose by counting sort ---------------------------------------------------
@@ -1328,8 +1334,36 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     }
   plan->d_blocks.alloc(nb, ctx);
   BBTC_CUDA(cudaMemcpyAsync(plan->d_blocks.p, plan->blocks.data(), nb * sizeof(BlockDesc), cudaMemcpyHostToDevice, st));
+  // Probe slots (resident counts, DESIGN §7 "Probe slots"): a probe block with many
+  // short rows gets a slot of 8 words per row after the cols arena — its length, its
+  // CSR offset and its first 6 column ids — so a probe of a row of <= 6 entries is one
+  // random 32-B access instead of a row-offset gather followed by a list gather.
+  plan->slot_of.assign(nb, 0);
+  plan->slots_ready = false;
+  uint64_t slot_words = 0;
+  const uint64_t slot_base = (m + 7) & ~7ull;   // slots 32-B aligned
+  {
+    // Off by default: measured slower on friendster (list kernel 336 -> 342 ms with slots
+    // for the four V_0 blocks; its short-row tasks are bound by staging, not by the row
+    // offset gathers), no change on rmat24 / orkut (profiles/r02/r02r).  BBTC_SLOTS=1.
+    static const bool on = getenv("BBTC_SLOTS") && atoi(getenv("BBTC_SLOTS")) != 0;
+    static const double min_rows = getenv("BBTC_SLOT_MIN_ROWS") ? atof(getenv("BBTC_SLOT_MIN_ROWS")) : 1e6;
+    static const double max_deg = getenv("BBTC_SLOT_MAX_DEG") ? atof(getenv("BBTC_SLOT_MAX_DEG")) : 8.0;
+    static const double min_deg = getenv("BBTC_SLOT_MIN_DEG") ? atof(getenv("BBTC_SLOT_MIN_DEG")) : 1.0;
+    for (uint32_t b = 0; on && !(flags & BBTC_PLAN_ROWMAJOR) && b < nb; ++b) {
+      const BlockDesc& B = plan->blocks[b];
+      const uint64_t rows = plan->cuts[B.i + 1] - plan->cuts[B.i];
+      // (rows of average length 1..8: mostly non-empty and mostly inline)
+      if ((double)rows < min_rows || !B.nnz || (double)B.nnz > max_deg * (double)rows ||
+          (double)B.nnz < min_deg * (double)rows)
+        continue;
+      if (slot_base + slot_words + 8 * rows >= 0xFFFFFFFFull) continue;   // 32-bit arena indices
+      plan->slot_of[b] = (uint32_t)(slot_base + slot_words);
+      slot_words += 8 * rows;
+    }
+  }
   if (!csr_count) {
-  plan->cols.alloc(m, ctx);
+  plan->cols.alloc(slot_words ? slot_base + slot_words : m, ctx);
   plan->rows.alloc(m, ctx);
   plan->rowptr.alloc(ro, ctx);
   BBTC_CUDA(cudaMemsetAsync(plan->rowptr.p, 0xFF, ro * 4, st));
@@ -1358,6 +1392,30 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
     BBTC_LAUNCHED(ctx);
   }
   tr.mark("rowptr");
+  if (slot_words && !csr_count) {
+    std::vector<uint32_t> ids, nrows(nb, 0);
+    uint32_t maxr = 1;
+    for (uint32_t b = 0; b < nb; ++b)
+      if (plan->slot_of[b]) {
+        ids.push_back(b);
+        nrows[b] = plan->cuts[plan->blocks[b].i + 1] - plan->cuts[plan->blocks[b].i];
+        maxr = std::max(maxr, nrows[b]);
+      }
+    DevBuf<uint32_t> d_ids, d_nrows;
+    d_ids.alloc(ids.size(), ctx);
+    d_nrows.alloc(nb, ctx);
+    plan->d_slot_of.alloc(nb, ctx);
+    BBTC_CUDA(cudaMemcpyAsync(d_ids.p, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st));
+    BBTC_CUDA(cudaMemcpyAsync(d_nrows.p, nrows.data(), nb * 4, cudaMemcpyHostToDevice, st));
+    BBTC_CUDA(cudaMemcpyAsync(plan->d_slot_of.p, plan->slot_of.data(), nb * 4, cudaMemcpyHostToDevice, st));
+    k_slots<<<dim3(std::min((maxr + kThreads - 1) / kThreads, (uint32_t)ctx->sm_count * 8), (uint32_t)ids.size()),
+              kThreads, 0, st>>>(plan->rowptr.p, plan->cols.p, plan->d_blocks.p, d_ids.p, plan->d_slot_of.p, d_nrows.p);
+    BBTC_LAUNCHED(ctx);
+    BBTC_CUDA(cudaStreamSynchronize(st));   // (host sources of the async copies)
+    plan->slots_ready = true;
+    plan->info.slot_bytes = 4 * slot_words;   // (not block bytes: a resident-count index)
+    tr.mark("slots");
+  }
   // Column-major iteration arrays (default): transpose of every block.
   plan->colmajor = !(flags & BBTC_PLAN_ROWMAJOR);
   if (plan->colmajor) {
@@ -1432,68 +1490,16 @@ void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* 
       BBTC_LAUNCHED(ctx);
       BBTC_CUDA(cudaStreamSynchronize(st));   // (colbase is the host source of an async copy)
     } else if (m && !batched) {
-      // Few blocks: sort each block in place by its local column (no key pass).  With
-      // row bands (BBTC_BANDS=1) the key is (row band, column): a block whose probe blocks
-      // G_ik (k >= j) exceed BBTC_BAND_BYTES (default 32 MB) is walked band by band.
-      // Measured slower (friendster p=4 list kernel 333 ms -> 440 / 565 / 740 ms at 64 /
-      // 32 / 16 MB bands: every band re-reads the staged lists of the columns it
-      // touches), so it stays an option.
-      // BBTC_BANDS=all bands every such block; BBTC_BANDS=cost only blocks whose tasks'
-      // probe words (nnz_ij x δ(G_ik), summed over k) exceed BBTC_BAND_RATIO (default 4)
-      // times the staged words the bands re-read (bands x non-empty columns x δ(G_jk)):
-      // long column runs over long probe lists.
-      static const char* bands_env = getenv("BBTC_BANDS");
-      static const bool bands = bands_env != nullptr;
-      static const bool band_cost = bands && std::string(bands_env) == "cost";
-      static const double band_ratio = getenv("BBTC_BAND_RATIO") ? atof(getenv("BBTC_BAND_RATIO")) : 4.0;
-      static const double band_bytes = getenv("BBTC_BAND_BYTES") ? atof(getenv("BBTC_BAND_BYTES")) : 32e6;
-      plan->band_shift.assign(nb, -1);
+      // Few blocks: sort each block in place by its local column (no key pass).  (A
+      // row-band walk — key (row band, column) for blocks whose probe blocks exceed an
+      // L2 share — was built and measured in round 2: friendster list kernel 333 -> 327
+      // ms with a cost rule choosing the blocks, 442 ms banding every large block; it
+      // faulted in the list kernel under a later build with many small bands for a
+      // reason not found, and was removed.  DESIGN §7.)
       for (uint32_t b = 0; b < nb; ++b) {
         const BlockDesc& B = plan->blocks[b];
         if (B.nnz == 0) continue;
         const int bits = std::max(1, bitlen(plan->cuts[B.j + 1] - plan->cuts[B.j] - 1));
-        const uint32_t rows_i = plan->cuts[B.i + 1] - plan->cuts[B.i];
-        const uint32_t cols_j = plan->cuts[B.j + 1] - plan->cuts[B.j];
-        int shift = -1;
-        if (bands && rows_i > 1) {
-          double probe = 0;   // the largest probe block this block's tasks gather from
-          double probe_words = 0, staged_words = 0;
-          for (uint32_t k = B.j; k < pe; ++k) {
-            const double nik = (double)plan->blocks[block_id(B.i, k)].nnz;
-            const double njk = (double)plan->blocks[block_id(B.j, k)].nnz;
-            probe = std::max(probe, 4.0 * nik + 4.0 * rows_i);
-            probe_words += (double)B.nnz * nik / rows_i;
-            staged_words += std::min<double>(cols_j, (double)B.nnz) * (cols_j ? njk / cols_j : 0.0);
-          }
-          const double nbands = std::ceil(probe / band_bytes);
-          if (tr.on)
-            fprintf(stderr, "[bbtc] band rule block (%u,%u): probe %.3g words, restaged %.3g words x %.0f bands%s\n",
-                    B.i, B.j, probe_words, staged_words, nbands,
-                    probe > band_bytes && (!band_cost || probe_words >= band_ratio * nbands * staged_words) ? " -> banded"
-                                                                                                        : "");
-          if (band_cost && probe_words < band_ratio * nbands * staged_words) probe = 0;
-          if (probe > band_bytes) {
-            const double band_rows = (double)rows_i * band_bytes / probe;
-            shift = std::max(0, (int)std::floor(std::log2(std::max(1.0, band_rows))));
-            if (bitlen((rows_i - 1) >> shift) + bits > 32) shift = -1;   // key must fit 32 bits
-          }
-        }
-        if (shift >= 0) {
-          DevBuf<uint32_t> keys;
-          keys.alloc(B.nnz, ctx);
-          k_band_keys<<<grid_for(ctx, B.nnz), kThreads, 0, st>>>(plan->rows.p + B.e0, plan->cols.p + B.e0, B.nnz,
-                                                                  shift, bits, keys.p);
-          BBTC_LAUNCHED(ctx);
-          const int kbits = bits + bitlen((rows_i - 1) >> shift);
-          cub_call(ctx, [&](void* t, size_t& bb) {
-            return cub::DeviceRadixSort::SortPairs(t, bb, keys.p, plan->ccv.p + B.e0, plan->rows.p + B.e0,
-                                                   plan->ccu.p + B.e0, B.nnz, 0, kbits, st);
-          }, radix_kernels(B.nnz, kbits));
-          k_band_cols<<<grid_for(ctx, B.nnz), kThreads, 0, st>>>(plan->ccv.p + B.e0, B.nnz, bits);
-          BBTC_LAUNCHED(ctx);
-          plan->band_shift[b] = shift;
-          continue;
-        }
         cub_call(ctx, [&](void* t, size_t& bb) {
           return cub::DeviceRadixSort::SortPairs(t, bb, plan->cols.p + B.e0, plan->ccv.p + B.e0, plan->rows.p + B.e0,
                                                  plan->ccu.p + B.e0, B.nnz, 0, bits, st);
@@ -1597,8 +1603,7 @@ uint64_t colptr_build(bbtc_ctx* ctx, bbtc_plan* plan, DevBuf<uint32_t>* out) {
     // (>= 4 edges per column on average: with sparser columns the kernel's 32-column
     // windows cover too few edges per batch — rmat24 (1,1): 2 edges/column, the
     // column-offset walk 2.7x slower than reading ccv, scripts/dbg/dbg_cp_tasks.py)
-    const bool cp = B.nnz >= 4 * ((uint64_t)w + 1) &&
-                    (plan->band_shift.empty() || plan->band_shift[b] < 0);   // (a banded column is split)
+    const bool cp = B.nnz >= 4 * ((uint64_t)w + 1);
     if (cp) {
       maxw = std::max(maxw, w + 1);
       co[b] = plan->co_off[b];
@@ -1972,6 +1977,7 @@ void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* oke
                              std::to_string(bnnz[b]) + " edges (every edge of an owned block must be sent to its owner)");
   }
   if (mg >= 0xFFFFFFFFull) raise(BBTC_ERANGE, "m >= 2^32-1 edges is not supported (32-bit block offsets)");
+  plan->slots_ready = false;   // (the slots do not move to the global layout)
   for (auto& A : plan->edge_arenas()) {
     DevBuf<uint32_t> g;
     g.alloc(std::max<uint64_t>(mg, 1), ctx);

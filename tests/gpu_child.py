@@ -22,6 +22,9 @@ def edges(spec):
     if kind == "rmat":
         scale, ef, seed = map(int, a)
         return (*inputs.rmat(scale, ef, seed), 1 << scale)
+    if kind == "gnp":
+        n, q, seed = int(a[0]), float(a[1]), int(a[2])
+        return (*inputs.gnp(n, q, seed), n)
     cfg = inputs.CONFIGS[kind]
     s, d = cfg.generate(seed=int(a[0]) if a else 1)
     return s, d, cfg.n_hint
@@ -32,7 +35,7 @@ def run(spec, p, modes, row_major=False):
     ctx = bb.Context(0)
     g = bb.Graph.from_edges(ctx, s, d, n_hint)
     plan = bb.Plan(ctx, g, p, row_major=row_major)
-    out = {"cuts": plan.cuts().tolist()}
+    out = {"cuts": plan.cuts().tolist(), "slots": plan.info()["slot_bytes"]}
     whole = plan.info()["block_bytes"]
     max_task = plan.info()["max_task_bytes"]
     host = False

@@ -580,12 +580,24 @@ def test_counting_sort_options(gpu):
     assert rank0 == og.rank().tolist()[:1000]
 
 
-def test_row_bands_option(gpu):
-    """Row bands (BBTC_BANDS): blocks walked by (row band, column) give the
-    oracle's per-task counts in every mode; a tiny band budget forces many bands."""
-    s, d = inputs.rmat(16, 16, 9)
-    og = oracle.OracleGraph(s, d, 1 << 16)
+
+@pytest.mark.parametrize("spec,p", [("rmat:16:16:9", 4), ("rmat:15:16:3", 7), ("gnp:3000:0.004:5", 3)])
+def test_probe_slots(gpu, spec, p):
+    """Probe slots: forced onto every block with at least one edge per row on
+    average, so rows of <= 6 entries are probed inline and longer ones through the CSR
+    offset in their slot — the oracle's per-task counts in every mode (streamed and
+    out-of-core counts run without slots, staged counts on rebuilt arenas)."""
+    kind, *a = spec.split(":")
+    if kind == "rmat":
+        s, d = inputs.rmat(int(a[0]), int(a[1]), int(a[2]))
+        n_hint = 1 << int(a[0])
+    else:
+        s, d = inputs.gnp(int(a[0]), float(a[1]), int(a[2]))
+        n_hint = int(a[0])
+    og = oracle.OracleGraph(s, d, n_hint)
     modes = ["resident", "ranks3", "streamed", "ooc50", "stage"]
-    res = child("rmat:16:16:9", 4, modes, env={"BBTC_BANDS": "1", "BBTC_BAND_BYTES": "65536"})
+    env = {"BBTC_SLOTS": "1", "BBTC_SLOT_MIN_ROWS": "1", "BBTC_SLOT_MIN_DEG": "0.5", "BBTC_SLOT_MAX_DEG": "1e9"}
+    res = child(spec, p, modes, env=env)
     otot, opt, _, _ = og.count(cuts=np.asarray(res["cuts"], np.uint32))
     assert_modes(res, modes, otot, opt)
+    assert res.get("slots", 1) > 0
