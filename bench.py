@@ -79,7 +79,9 @@ def live_traffic(cfg, p, seed, timeout=900):
     with tempfile.TemporaryDirectory() as tmp:
         log = os.path.join(tmp, "ncu.csv")
         cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
-               "lts__t_sector_hit_rate.pct", "--clock-control", "none", "-k", "regex:k_count", "--csv",
+               "lts__t_sector_hit_rate.pct,smsp__inst_executed.sum,l1tex__throughput.avg.pct_of_peak_sustained_elapsed,"
+               "lts__throughput.avg.pct_of_peak_sustained_elapsed,smsp__issue_active.avg.pct_of_peak_sustained_active",
+               "--clock-control", "none", "-k", "regex:k_count", "--csv",
                "--log-file", log, sys.executable, os.path.join(ROOT, "scripts", "profile_count.py"), cfg.name,
                str(p), str(seed)]
         try:
@@ -108,6 +110,10 @@ def live_traffic(cfg, p, seed, timeout=900):
         out[kind] = {"dram_bytes": d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0),
                      "dram_read_bytes": d.get("dram__bytes_read.sum", 0),
                      "ncu_ms": d.get("gpu__time_duration.sum"), "l2_hit_pct": d.get("lts__t_sector_hit_rate.pct"),
+                     "warp_inst": d.get("smsp__inst_executed.sum"),
+                     "l1tex_pct": d.get("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "l2_pct": d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "issue_active_pct": d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                      "launch_id": lid}
     return out, "ncu " + " ".join(cmd[1:9])
 
@@ -577,6 +583,17 @@ def main():
                       "l2_hit_pct": tr["l2_hit_pct"], "ncu_ms_cold_serialised": tr["ncu_ms"],
                       "traffic_over_compulsory": tr["dram_bytes"] / compulsory if compulsory else None})
             d["frac"] = d["achieved"] / peak
+            # the other limits the kernel runs into (ncu, same launch): warp instructions
+            # issued per second of the CUDA-event time against the SMs x 4 schedulers x the
+            # measured SM clock, and ncu's L1/TEX and L2 throughput fractions
+            sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+            if tr.get("warp_inst"):
+                peak_issue = torch.cuda.get_device_properties(local).multi_processor_count * 4 * sm_mhz * 1e6
+                d["issue"] = {"warp_inst": tr["warp_inst"], "rate": tr["warp_inst"] / (t_ms / 1e3),
+                              "peak": peak_issue, "frac": tr["warp_inst"] / (t_ms / 1e3) / peak_issue,
+                              "ncu_issue_active_pct": tr.get("issue_active_pct")}
+            d["ncu_l1tex_pct"] = tr.get("l1tex_pct")
+            d["ncu_l2_pct"] = tr.get("l2_pct")
         if b_alg is not None:
             d["b_alg_bytes"] = b_alg
             d["b_alg_logical_frac"] = b_alg / (t_ms / 1e3) / 1e9 / peak if t_ms > 0 else None
