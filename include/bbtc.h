@@ -152,6 +152,31 @@ BBTC_API void bbtc_edges_free(bbtc_edge_list* e);
 BBTC_API bbtc_status bbtc_graph_load(bbtc_ctx* ctx, const char* path, int format, uint32_t n_hint,
                                      bbtc_graph** out);
 
+/* Memory-mapped host source (graphs larger than memory are read through
+ * memory-mapped files).  bbtc_edges_map maps a BBTC_FMT_BIN file read-only — nothing is
+ * copied into library memory; the page cache brings the pages in as the graph build's
+ * chunked host->device copies read them, so the raw list need not fit in RAM.
+ * pairs = the file's interleaved uint32 pairs (n_edges of them); base/bytes = the
+ * mapping (release with bbtc_edges_unmap, after the graph is built).
+ * Errors: BBTC_EINVAL (NULL path/out), BBTC_EIO (open/stat/mmap failure), BBTC_EPARSE
+ * (size not a multiple of 8). */
+typedef struct {
+  const uint32_t* pairs;   /* host, 2 * n_edges entries: src0 dst0 src1 dst1 … (read-only mapping) */
+  uint64_t n_edges;
+  void* base;              /* the mapping (NULL for an empty file) */
+  uint64_t bytes;
+} bbtc_edge_map;
+BBTC_API bbtc_status bbtc_edges_map(const char* path, bbtc_edge_map* out);
+BBTC_API void bbtc_edges_unmap(bbtc_edge_map* m);
+/* bbtc_graph_from_edges for interleaved pairs (src0 dst0 src1 dst1 …, the binary edge
+ * file layout) in host (mem = BBTC_MEM_HOST, pinned, pageable or memory-mapped) or device
+ * memory.  Same result and errors as bbtc_graph_from_edges on the split arrays. */
+BBTC_API bbtc_status bbtc_graph_from_pairs(bbtc_ctx* ctx, const uint32_t* pairs, uint64_t n_edges, uint32_t n_hint,
+                                           int mem, bbtc_graph** out);
+/* bbtc_edges_map + bbtc_graph_from_pairs(…, BBTC_MEM_HOST) + bbtc_edges_unmap: a graph
+ * from a binary edge file that is never read whole into RAM.  Errors: those of both. */
+BBTC_API bbtc_status bbtc_graph_load_mapped(bbtc_ctx* ctx, const char* path, uint32_t n_hint, bbtc_graph** out);
+
 /* ------------------------------------------------------------------- plan */
 typedef struct {
   uint32_t p;               /* parts after clamping (p > n -> n; n == 0 -> 1) */

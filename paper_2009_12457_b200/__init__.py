@@ -21,7 +21,7 @@ from . import _lib as L
 from ._lib import BBTCError, MEM_DEVICE, MEM_HOST, PLAN_STATS
 
 __all__ = ["Context", "Graph", "Plan", "BBTCError", "n_tasks", "task_index", "task_ijk", "count_triangles",
-           "read_edges", "FORMATS", "auto_p"]
+           "read_edges", "EdgeMap", "FORMATS", "auto_p"]
 
 FORMATS = {"text": L.FMT_TEXT, "mm": L.FMT_MM, "bin": L.FMT_BIN}
 
@@ -37,6 +37,34 @@ def read_edges(path, fmt: str = "text"):
         return src, dst, int(e.n_hint)
     finally:
         L.bbtc_edges_free(ctypes.byref(e))
+
+
+class EdgeMap:
+    """bbtc_edges_map: a binary edge file (interleaved uint32 pairs) memory-mapped
+    read-only; `pairs` is an (n_edges, 2) numpy view of the mapping (valid until close)."""
+
+    def __init__(self, path):
+        self._m = L.bbtc_edge_map()
+        L.check(L.bbtc_edges_map(str(path).encode(), ctypes.byref(self._m)))
+        n = int(self._m.n_edges)
+        self.n_edges = n
+        self.pairs = (np.ctypeslib.as_array(self._m.pairs, shape=(n, 2)) if n
+                      else np.empty((0, 2), np.uint32))
+
+    def close(self):
+        if getattr(self, "_m", None) is not None and L is not None and L.lib is not None:
+            self.pairs = None
+            L.bbtc_edges_unmap(ctypes.byref(self._m))
+        self._m = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        self.close()
 
 
 def _ptr(x, want_dtype):
@@ -147,6 +175,32 @@ class Graph:
         assert ps[2] == pd[2], "src and dst must both be host or both device"
         h = ctypes.c_void_p()
         L.check(L.bbtc_graph_from_edges(ctx.handle, ps[0], pd[0], ps[1], n_hint, ps[2], ctypes.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def from_pairs(cls, ctx: Context, pairs, n_hint: int = 0) -> "Graph":
+        """bbtc_graph_from_pairs: interleaved (n, 2) uint32 pairs, host (numpy, incl. an
+        EdgeMap's mapping) or device (CUDA tensor)."""
+        if hasattr(pairs, "data_ptr"):
+            assert pairs.dim() == 2 and pairs.shape[1] == 2, "pairs must be (n, 2)"
+            ptr, n, mem = _ptr(pairs.reshape(-1), np.uint32)[:3]
+            n //= 2
+        else:
+            a = np.asarray(pairs)
+            assert a.ndim == 2 and a.shape[1] == 2, "pairs must be (n, 2)"
+            if not (a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]):
+                a = _ptr(a.reshape(-1), np.uint32)[3].reshape(-1, 2)
+            ptr, n, mem = ctypes.c_void_p(a.ctypes.data), a.shape[0], MEM_HOST
+        h = ctypes.c_void_p()
+        L.check(L.bbtc_graph_from_pairs(ctx.handle, ptr, n, n_hint, mem, ctypes.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def load_mapped(cls, ctx: Context, path, n_hint: int = 0) -> "Graph":
+        """bbtc_graph_load_mapped: a binary edge file, memory-mapped (never read whole
+        into RAM), built into the graph (a1-a2)."""
+        h = ctypes.c_void_p()
+        L.check(L.bbtc_graph_load_mapped(ctx.handle, str(path).encode(), n_hint, ctypes.byref(h)))
         return cls(ctx, h)
 
     @classmethod

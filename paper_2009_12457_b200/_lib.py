@@ -63,6 +63,10 @@ class bbtc_edge_list(ctypes.Structure):
     _fields_ = [("src", _u32p), ("dst", _u32p), ("n_edges", c_u64), ("n_hint", c_u32), ("reserved", c_u32)]
 
 
+class bbtc_edge_map(ctypes.Structure):
+    _fields_ = [("pairs", _u32p), ("n_edges", c_u64), ("base", _vp), ("bytes", c_u64)]
+
+
 class bbtc_timing(ctypes.Structure):
     _fields_ = [("t_total_ms", ctypes.c_double), ("t_h2d_ms", ctypes.c_double), ("t_kernel_ms", ctypes.c_double),
                 ("h2d_bytes", c_u64), ("launches", c_u64), ("t_dense_ms", ctypes.c_double)]
@@ -104,6 +108,10 @@ bbtc_graph_free = _sig("bbtc_graph_free", None, _vp)
 bbtc_edges_read = _sig("bbtc_edges_read", _st, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(bbtc_edge_list))
 bbtc_edges_free = _sig("bbtc_edges_free", None, ctypes.POINTER(bbtc_edge_list))
 bbtc_graph_load = _sig("bbtc_graph_load", _st, _vp, ctypes.c_char_p, ctypes.c_int, c_u32, _pp)
+bbtc_edges_map = _sig("bbtc_edges_map", _st, ctypes.c_char_p, ctypes.POINTER(bbtc_edge_map))
+bbtc_edges_unmap = _sig("bbtc_edges_unmap", None, ctypes.POINTER(bbtc_edge_map))
+bbtc_graph_from_pairs = _sig("bbtc_graph_from_pairs", _st, _vp, _vp, c_u64, c_u32, ctypes.c_int, _pp)
+bbtc_graph_load_mapped = _sig("bbtc_graph_load_mapped", _st, _vp, ctypes.c_char_p, c_u32, _pp)
 bbtc_plan_create = _sig("bbtc_plan_create", _st, _vp, _vp, c_u32, _u32p, c_u32, _pp)
 bbtc_plan_auto_p = _sig("bbtc_plan_auto_p", _st, _vp, _vp, c_u64, c_u32, c_u32, _u32p)
 bbtc_plan_info_get = _sig("bbtc_plan_info_get", _st, _vp, ctypes.POINTER(bbtc_plan_info))

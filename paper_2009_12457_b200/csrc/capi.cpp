@@ -725,6 +725,26 @@ BBTC_API bbtc_status bbtc_graph_from_edges(bbtc_ctx* ctx, const uint32_t* src, c
   });
 }
 
+BBTC_API bbtc_status bbtc_graph_from_pairs(bbtc_ctx* ctx, const uint32_t* pairs, uint64_t n_edges, uint32_t n_hint,
+                                           int mem, bbtc_graph** out) {
+  return guard([&] {
+    if (!ctx || !out) raise(BBTC_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+    if (n_edges && !pairs) raise(BBTC_EINVAL, "pairs is NULL");
+    if (mem != BBTC_MEM_HOST && mem != BBTC_MEM_DEVICE) raise(BBTC_EINVAL, "mem must be BBTC_MEM_HOST or _DEVICE");
+    BBTC_CUDA(cudaSetDevice(ctx->device));
+    auto* g = new bbtc_graph();
+    g->ctx = ctx;
+    try {
+      graph_build(ctx, nullptr, nullptr, n_edges, n_hint, mem, g, n_edges ? pairs : nullptr);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
 BBTC_API bbtc_status bbtc_graph_stats_get(const bbtc_graph* g, bbtc_graph_stats* s) {
   return guard([&] {
     if (!g || !s) raise(BBTC_EINVAL, "NULL argument");

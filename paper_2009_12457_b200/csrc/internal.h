@@ -250,7 +250,7 @@ struct bbtc_plan {
 namespace bbtc {
 // prep.cu
 void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint,
-                 int mem, bbtc_graph* g);
+                 int mem, bbtc_graph* g, const uint32_t* pairs = nullptr);   // pairs: interleaved src/dst
 void graph_csr(bbtc_ctx* ctx, const bbtc_graph* g, uint64_t* row_ptr, uint32_t* col);
 uint32_t graph_dplus_max(bbtc_graph* g);
 void plan_build(bbtc_ctx* ctx, const bbtc_graph* g, uint32_t p, const uint32_t* user_cuts, uint32_t flags,

@@ -14,6 +14,11 @@
 #include <string>
 #include <vector>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include "internal.h"
 
 namespace bbtc {
@@ -220,6 +225,62 @@ BBTC_API void bbtc_edges_free(bbtc_edge_list* e) {
   free(e->src);
   free(e->dst);
   *e = bbtc_edge_list{};
+}
+
+BBTC_API bbtc_status bbtc_edges_map(const char* path, bbtc_edge_map* out) {
+  return guarded([&] {
+    if (!path || !out) raise(BBTC_EINVAL, "path/out is NULL");
+    *out = bbtc_edge_map{};
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) raise(BBTC_EIO, std::string(path) + ": " + strerror(errno));
+    struct stat stt;
+    if (fstat(fd, &stt) != 0) {
+      const int er = errno;
+      close(fd);
+      raise(BBTC_EIO, std::string(path) + ": " + strerror(er));
+    }
+    const uint64_t bytes = (uint64_t)stt.st_size;
+    if (bytes % 8) {
+      close(fd);
+      raise(BBTC_EPARSE, std::string(path) + ": binary edge file size " + std::to_string(bytes) +
+                             " is not a multiple of 8");
+    }
+    void* base = nullptr;
+    if (bytes) {
+      base = mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE | MAP_NORESERVE, fd, 0);
+      if (base == MAP_FAILED) {
+        const int er = errno;
+        close(fd);
+        raise(BBTC_EIO, std::string(path) + ": mmap: " + strerror(er));
+      }
+      madvise(base, bytes, MADV_SEQUENTIAL);   // read once, front to back, by the chunked H2D
+    }
+    close(fd);   // (the mapping stays valid)
+    out->pairs = static_cast<const uint32_t*>(base);
+    out->n_edges = bytes / 8;
+    out->base = base;
+    out->bytes = bytes;
+  });
+}
+
+BBTC_API void bbtc_edges_unmap(bbtc_edge_map* m) {
+  if (!m) return;
+  if (m->base && m->bytes) munmap(m->base, m->bytes);
+  *m = bbtc_edge_map{};
+}
+
+BBTC_API bbtc_status bbtc_graph_load_mapped(bbtc_ctx* ctx, const char* path, uint32_t n_hint, bbtc_graph** out) {
+  bbtc_status st = guarded([&] {
+    if (!ctx || !out) raise(BBTC_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+  });
+  if (st != BBTC_OK) return st;
+  bbtc_edge_map M{};
+  st = bbtc_edges_map(path, &M);
+  if (st != BBTC_OK) return st;
+  st = bbtc_graph_from_pairs(ctx, M.pairs, M.n_edges, n_hint, BBTC_MEM_HOST, out);
+  bbtc_edges_unmap(&M);
+  return st;
 }
 
 BBTC_API bbtc_status bbtc_graph_load(bbtc_ctx* ctx, const char* path, int format, uint32_t n_hint,

@@ -111,6 +111,21 @@ __global__ void k_canon(const uint32_t* __restrict__ src, const uint32_t* __rest
   if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
 }
 
+// The same for interleaved input pairs (src0 dst0 src1 dst1 …: a binary edge file
+// as stored, e.g. memory-mapped by bbtc_edges_map).
+__global__ void k_canon_pairs(const uint2* __restrict__ pairs, uint64_t E, int bw, uint64_t* __restrict__ keys,
+                              uint32_t* __restrict__ max_id) {
+  uint32_t mx = 0;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < E; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 q = pairs[e];
+    const uint32_t lo = min(q.x, q.y), hi = max(q.x, q.y);
+    mx = max(mx, hi);
+    keys[e] = q.x == q.y ? kSentinel : ((uint64_t)lo << bw) | hi;
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(max_id, mx);
+}
+
 // Hash-set canonicalisation: every raw pair's key (min << bw | max) is inserted into
 // an open-addressing table of 2^k u64 slots (load <= 1/2, linear probing); the
 // table then holds each undirected edge once (duplicates and both orientations
@@ -892,7 +907,7 @@ static bool bucket_unique(bbtc_ctx* ctx, const uint64_t* keys, uint64_t E, int K
 
 // =====================================================================================
 void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64_t E, uint32_t n_hint, int mem,
-                 bbtc_graph* g) {
+                 bbtc_graph* g, const uint32_t* pairs) {
   cudaStream_t st = ctx->stream;
   Trace tr(st, "graph_build");
   g->raw = E;
@@ -919,7 +934,11 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
   }
   int bw = n_hint > 1 ? std::max(1, bitlen(n_hint - 1)) : 32;
   auto launch_canon = [&](const uint32_t* s, const uint32_t* d, uint64_t len, uint64_t c0, int width) {
-    if (use_hash)
+    if (pairs) {   // interleaved pairs: s points at the chunk's first pair, d is unused
+      if (use_hash) raise(BBTC_EINVAL, "BBTC_DEDUP=hash takes separate src/dst arrays");
+      k_canon_pairs<<<grid_for(ctx, len), kThreads, 0, st>>>(reinterpret_cast<const uint2*>(s), len, width,
+                                                             keys.p + c0, dmax.p);
+    } else if (use_hash)
       k_canon_insert<<<grid_for(ctx, len), kThreads, 0, st>>>(s, d, len, width, table.p, tbits, dmax.p);
     else
       k_canon<<<grid_for(ctx, len), kThreads, 0, st>>>(s, d, len, width, keys.p + c0, dmax.p);
@@ -959,14 +978,14 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     if (use_hash) BBTC_CUDA(cudaMemsetAsync(table.p, 0xFF, (1ull << tbits) * 8, st));
     if (!E) return;
     if (mem == BBTC_MEM_DEVICE) {
-      launch_canon(src, dst, E, 0, width);
+      launch_canon(pairs ? pairs : src, dst, E, 0, width);
       return;
     }
     // Host input: chunked H2D on a copy stream, overlapped with k_canon on earlier chunks.
     const uint64_t chunk = 1ull << 25;   // 32 Mi pairs = 256 MiB per chunk
     DevBuf<uint32_t> ds, dd;
-    ds.alloc(std::min(E, 2 * chunk), ctx);
-    dd.alloc(std::min(E, 2 * chunk), ctx);
+    ds.alloc(std::min(E, 2 * chunk) * (pairs ? 2 : 1), ctx);   // (interleaved pairs: 8 B each, in ds)
+    if (!pairs) dd.alloc(std::min(E, 2 * chunk), ctx);
     cudaStream_t cs = ctx->copy_streams[0];
     cudaEvent_t ev_copied[2], ev_used[2];
     for (int x = 0; x < 2; ++x) {
@@ -979,11 +998,16 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       const uint64_t len = std::min(chunk, E - c0);
       const int slot = it & 1;
       BBTC_CUDA(cudaStreamWaitEvent(cs, ev_used[slot], 0));
-      BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
-      BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
+      if (pairs) {
+        BBTC_CUDA(cudaMemcpyAsync(ds.p + 2 * slot * chunk, pairs + 2 * c0, len * 8, cudaMemcpyHostToDevice, cs));
+      } else {
+        BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
+        BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
+      }
       BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
       BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
-      launch_canon(ds.p + slot * chunk, dd.p + slot * chunk, len, c0, width);
+      if (pairs) launch_canon(ds.p + 2 * slot * chunk, nullptr, len, c0, width);
+      else launch_canon(ds.p + slot * chunk, dd.p + slot * chunk, len, c0, width);
       BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
       // Stream-sort: once a sort piece is complete, sort it on the aux stream while
       // the next pieces are still crossing PCIe.

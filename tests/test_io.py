@@ -170,3 +170,51 @@ def test_text_and_mm_roundtrip_random(tmp_path):
         np.savetxt(f, np.stack([s.astype(np.uint64) + 1, d.astype(np.uint64) + 1, np.ones_like(s)], 1), fmt="%d")
     ms, md, nh = bb.read_edges(m, "mm")
     assert nh == n and np.array_equal(ms, s) and np.array_equal(md, d)
+
+
+def test_edges_map_matches_read(tmp_path):
+    """bbtc_edges_map (memory-mapped host source): the mapping of a binary
+    file holds exactly the pairs bbtc_edges_read parses; empty and odd-sized files."""
+    bb = _bb()
+    s, d = inputs.rmat(11, 16, seed=5)
+    p = tmp_path / "m.bin"
+    write_bin(p, s, d)
+    with bb.EdgeMap(p) as m:
+        assert m.n_edges == len(s)
+        assert np.array_equal(m.pairs[:, 0], s) and np.array_equal(m.pairs[:, 1], d)
+    e = tmp_path / "empty.bin"
+    e.write_bytes(b"")
+    with bb.EdgeMap(e) as m:
+        assert m.n_edges == 0 and m.pairs.shape == (0, 2)
+    o = tmp_path / "odd.bin"
+    o.write_bytes(b"\x00" * 12)
+    with pytest.raises(bb.BBTCError) as ei:
+        bb.EdgeMap(o)
+    assert ei.value.code == -4
+    with pytest.raises(bb.BBTCError) as ei:
+        bb.EdgeMap(tmp_path / "nope.bin")
+    assert ei.value.code == -3
+
+
+@pytest.mark.gpu
+def test_graph_from_pairs_and_mapped_file(tmp_path):
+    """Interleaved pairs (host numpy, a memory-mapped file, a CUDA tensor) build the same
+    graph as the split arrays: same n, m and the oracle's per-task counts."""
+    import torch
+    bb = _bb()
+    s, d = inputs.rmat(14, 16, seed=4)
+    p = tmp_path / "r14.bin"
+    write_bin(p, s, d)
+    og = oracle.OracleGraph(s, d, 1 << 14)
+    ot, opt, _, _ = og.count(5)
+    ctx = bb.Context(0)
+    pairs = np.stack([s, d], axis=1)
+    graphs = [bb.Graph.from_pairs(ctx, pairs, 1 << 14),
+              bb.Graph.load_mapped(ctx, p, 1 << 14),
+              bb.Graph.from_pairs(ctx, torch.from_numpy(pairs.view(np.int32)).cuda(), 1 << 14)]
+    with bb.EdgeMap(p) as m:
+        graphs.append(bb.Graph.from_pairs(ctx, m.pairs, 1 << 14))
+    for g in graphs:
+        assert g.size() == (og.n, og.m)
+        total, per_task = bb.Plan(ctx, g, 5).count()
+        assert total == ot and np.array_equal(per_task, opt)
