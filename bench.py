@@ -541,9 +541,11 @@ def main():
     t_x = [r[2]["t_total_ms"] for r in reps_x]
     t_i = [r[2]["t_total_ms"] for r in reps_i]
     t_h2d = [r[2]["t_h2d_ms"] for r in reps_i]
-    # Out of core: the device may hold only half of the blocks.
+    # Out of core: the device may hold only half of the blocks (or just the
+    # largest task's three blocks where that is more: small p).
     plan.unstage()
-    plan.set_budget(pinfo["block_bytes"] // 2)
+    ooc_budget = max(pinfo["block_bytes"] // 2, int(pinfo["max_task_bytes"] * 1.05))
+    plan.set_budget(ooc_budget)
     plan.count(rank, world)                      # first use of the cache arenas' sizes
     tot_o, _, tm_o = plan.count(rank, world, timing=True)
     # Streaming (unlock order) and the budget re-order the tasks, so a rank's share of
@@ -641,6 +643,7 @@ def main():
                          "count_excl_h2d": statistics.median(t_x), "count_incl_h2d": statistics.median(t_i),
                          "h2d_bytes_blocks": tm_i["h2d_bytes"],
                          "count_out_of_core_half_budget": tm_o["t_total_ms"], "h2d_bytes_out_of_core": tm_o["h2d_bytes"],
+                         "out_of_core_budget_bytes": ooc_budget,
                          "gen_s": t_gen},
         "plan": {"lambda": pinfo["lambda"], "dmax_blk": pinfo["dmax_blk"], "visits": pinfo["visits"],
                  "b_alg": pinfo["b_alg"], "work_items": pinfo["work_items"], "block_bytes": pinfo["block_bytes"],

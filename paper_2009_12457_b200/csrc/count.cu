@@ -77,6 +77,9 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 #ifndef BBTC_P1_DEPTH
 #define BBTC_P1_DEPTH 4   // A/B: 8 = rounds of eight 32-word loads in flight for long probe lists
 #endif
+#ifndef BBTC_DENSE_LIVE
+#define BBTC_DENSE_LIVE 1   // bit-row kernel: skip the loads past a row's live uint4 (A/B: 0 = load the full stride)
+#endif
 #ifndef BBTC_DEBUG_BOUNDS
 #define BBTC_DEBUG_BOUNDS 0   // debug builds: bounds checks in the list kernel (report via mapped host memory)
 #endif
@@ -732,7 +735,9 @@ __global__ void k_dense_rows(const uint32_t* __restrict__ it_u, const uint32_t* 
 template <int S, bool kKeepU>
 __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
                                                 const uint32_t* __restrict__ Dik, const uint32_t* __restrict__ Djk,
-                                                uint64_t e_begin, uint64_t e_end, int lane) {
+                                                uint64_t e_begin, uint64_t e_end, int lane, uint32_t live) {
+  // live = uint4 of a row that hold bits of V_k (ceil(|V_k| / 128)); the stride S is the
+  // next power of two: loads past the live part are skipped (they only read zeros).
   constexpr int kV = S / 4;                      // uint4 per row
   constexpr int LPR = kV < 32 ? kV : 32;         // lanes per edge
   constexpr int Q = kV / LPR;                    // uint4 per lane per row
@@ -763,7 +768,7 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
         const bool fresh = !kKeepU || uu != ku;
 #pragma unroll
         for (int x = 0; x < Q; ++x) {
-          if (idx < n) {
+          if (idx < n && (uint32_t)(q + x * LPR) < live) {
             a[r][x] = fresh ? Di[(uint64_t)uu * kV + x * LPR] : ka[x];
             b[r][x] = Dj[(uint64_t)vv * kV + x * LPR];
           } else {
@@ -821,14 +826,15 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
     const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * T.chunk;
     const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
     uint32_t acc = 0;
+    const uint32_t live = BBTC_DENSE_LIVE ? (blocks[T.jk].nc + 127) / 128 : 0xFFFFFFFFu;   // |V_k| = columns of G_jk
     switch (T.pad) {
-      case 8: acc = dense_edges<8, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 16: acc = dense_edges<16, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 32: acc = dense_edges<32, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 64: acc = dense_edges<64, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 128: acc = dense_edges<128, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      case 256: acc = dense_edges<256, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
-      default: acc = dense_edges<512, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 8: acc = dense_edges<8, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 16: acc = dense_edges<16, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 32: acc = dense_edges<32, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 64: acc = dense_edges<64, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 128: acc = dense_edges<128, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 256: acc = dense_edges<256, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      default: acc = dense_edges<512, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
     }
     const uint32_t s = __reduce_add_sync(kFull, acc);
     if (lane == 0 && s) {
