@@ -78,7 +78,10 @@ __device__ __forceinline__ T ld_stream(const T* p) {
 #define BBTC_P1_DEPTH 4   // A/B: 8 = rounds of eight 32-word loads in flight for long probe lists
 #endif
 #ifndef BBTC_DENSE_LIVE
-#define BBTC_DENSE_LIVE 1   // bit-row kernel: skip the loads past a row's live uint4 (A/B: 0 = load the full stride)
+// A/B: the bit-row kernel skips the loads past a row's live uint4 (|V_k| bits of a
+// power-of-two stride): measured slower (rmat24 p=10 bit-row kernel 11.44 -> 12.18 ms,
+// orkut 1.15 -> 1.26; profiles/r02/r02u), so the full stride is loaded.
+#define BBTC_DENSE_LIVE 0
 #endif
 #ifndef BBTC_DEBUG_BOUNDS
 #define BBTC_DEBUG_BOUNDS 0   // debug builds: bounds checks in the list kernel (report via mapped host memory)
@@ -101,6 +104,9 @@ __device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long lon
   } while (0)
 #else
 #define DBG_CHECK(cond, code, a, b, c, d, e, f, g) do { } while (0)
+#endif
+#ifndef BBTC_P1_UNIFIED
+#define BBTC_P1_UNIFIED 1   // phase 1: the last < 4 rounds of a long list in one predicated round
 #endif
 #ifndef BBTC_PF_NEXT
 #define BBTC_PF_NEXT 0   // A/B: rolling L2 prefetch of the next long probe list and of the remainders
@@ -290,10 +296,20 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
       for (int x = 0; x < 8; ++x) hits += test(w[x], sl);
     }
 #endif
+#if BBTC_P1_UNIFIED
+    // Rounds of up to four 32-word loads in flight, the last one predicated: a list of
+    // 32-127 words costs one load latency instead of one per round.
+    for (; off < nfull; off += 128) {
+      const bool h2 = off + 32 < nfull, h3 = off + 64 < nfull, h4 = off + 96 < nfull;
+      const uint32_t w1 = B[off], w2 = h2 ? B[off + 32] : 0u, w3 = h3 ? B[off + 64] : 0u, w4 = h4 ? B[off + 96] : 0u;
+      hits += test(w1, sl) + (h2 ? test(w2, sl) : 0u) + (h3 ? test(w3, sl) : 0u) + (h4 ? test(w4, sl) : 0u);
+    }
+#else
     for (; off + 128 <= nfull; off += 128) {
       const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
       hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
     }
+#endif
 #if BBTC_TAIL3
     // the last 0-3 full rounds with their loads issued together (lists of 32-127 words
     // otherwise wait out one load latency per round)
