@@ -108,6 +108,7 @@ __device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long lon
 #ifndef BBTC_P1_UNIFIED
 #define BBTC_P1_UNIFIED 1   // phase 1: the last < 4 rounds of a long list in one predicated round
 #endif
+constexpr bool kP1Unified = BBTC_P1_UNIFIED;
 #ifndef BBTC_PF_NEXT
 #define BBTC_PF_NEXT 0   // A/B: rolling L2 prefetch of the next long probe list and of the remainders
 #endif
@@ -254,7 +255,7 @@ __device__ __forceinline__ uint32_t table_probe(const uint32_t* tab, uint32_t hk
 // a time in whole 32-word rounds (all lanes on consecutive words of one list, four
 // loads in flight); phase 2 flattens the < 32-word remainders across the lanes.
 // test(w, slot) = 1 if probe word w of a lane whose staged list has slot `slot` is in it.
-template <class Test>
+template <bool kUnified, class Test>
 __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ cols, uint2* pay, int lane, uint32_t bx,
                                                 uint32_t bl, uint32_t slot, Test test) {
   uint32_t hits = 0;
@@ -296,20 +297,23 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
       for (int x = 0; x < 8; ++x) hits += test(w[x], sl);
     }
 #endif
-#if BBTC_P1_UNIFIED
-    // Rounds of up to four 32-word loads in flight, the last one predicated: a list of
-    // 32-127 words costs one load latency instead of one per round.
+    // kUnified: rounds of up to four 32-word loads in flight, the last one predicated —
+    // a list of 32-127 words costs one load latency instead of one per round.  In the
+    // hash-only kernel variant (friendster 336.4 -> 331.4 ms); the bitmap variant, tighter
+    // on registers, measured slower with it (rmat24 31.9 -> 32.2, orkut 11.89 -> 12.11;
+    // profiles/r02/r02w).
+    if constexpr (kUnified) {
     for (; off < nfull; off += 128) {
       const bool h2 = off + 32 < nfull, h3 = off + 64 < nfull, h4 = off + 96 < nfull;
       const uint32_t w1 = B[off], w2 = h2 ? B[off + 32] : 0u, w3 = h3 ? B[off + 64] : 0u, w4 = h4 ? B[off + 96] : 0u;
       hits += test(w1, sl) + (h2 ? test(w2, sl) : 0u) + (h3 ? test(w3, sl) : 0u) + (h4 ? test(w4, sl) : 0u);
     }
-#else
+    } else {
     for (; off + 128 <= nfull; off += 128) {
       const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
       hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
     }
-#endif
+    }
 #if BBTC_TAIL3
     // the last 0-3 full rounds with their loads issued together (lists of 32-127 words
     // otherwise wait out one load latency per round)
@@ -358,6 +362,7 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
 // when slot tags do not fit in 32 bits), hashed alone with untagged keys in chunks
 // of kChunk words.  |S ∩ P| is additive over a partition of S, so every probe list
 // is probed once per chunk.  Returns this lane's hits.
+template <bool kUnified>
 __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ cS,
                                            uint32_t s0, uint32_t total_a, uint32_t bx, uint32_t bl, uint32_t* tab,
                                            uint2* pay, int lane) {
@@ -372,7 +377,7 @@ __device__ __noinline__ uint32_t long_list(const uint32_t* __restrict__ cols, co
     __syncwarp();
     for (uint32_t x = lane; x < cn; x += 32) table_insert<4>(tab, ld_stream(cS + s0 + c0 + x), G);
     __syncwarp();
-    hits += probe_lists(cols, pay, lane, bx, bl, 0,
+    hits += probe_lists<kUnified>(cols, pay, lane, bx, bl, 0,
                         [&](uint32_t w, uint32_t) { return table_probe<4>(tab, w, G); });
   }
   return hits;
@@ -622,7 +627,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                 if (ok_nxt && alen > 0) probe_of(p_nxt, xn, bln);
                 ok_nn = edge(e2 + 64, p_nn);
               }
-              hits += probe_lists(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
+              hits += probe_lists<kP1Unified && !kBm>(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
               e2 += 32;
@@ -640,7 +645,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
               if (L2 == 0) break;
               uint32_t x2 = 0, bl2 = 0;
               if (ok && alen > 0) probe_of(kCol ? it_u[e2] : it_v[e2], x2, bl2);
-              hits += probe_lists(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
+              hits += probe_lists<kP1Unified && !kBm>(cols, pay, lane, x2, lane < L2 ? bl2 : 0u, 0, test);
               L += L2;
               if (L2 < 32) break;
           }
@@ -676,10 +681,10 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
           }
           __syncwarp();
           auto test = [bm](uint32_t w, uint32_t base_w) { return (bm[base_w + (w >> 5)] >> (w & 31)) & 1u; };
-          hits += probe_lists(cols, pay, lane, bx, bl, slot * bmw, test);
+          hits += probe_lists<kP1Unified && !kBm>(cols, pay, lane, bx, bl, slot * bmw, test);
           continue_run(test);
         } else if (longl) {
-          hits += long_list(cols, cS, __shfl_sync(kFull, a0, 0), __shfl_sync(kFull, alen, 0), bx, bl, tab, pay,
+          hits += long_list<kP1Unified && !kBm>(cols, cS, __shfl_sync(kFull, a0, 0), __shfl_sync(kFull, alen, 0), bx, bl, tab, pay,
                             lane);
         } else {
           // ---- stage the distinct lists S of lanes [0,L) into one table
@@ -699,7 +704,7 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                   [&](uint32_t, uint2 P, uint32_t w) { table_insert<BW>(tab, (w << 5) | P.y, G); });
           // ---- probe every word of each lane's list P against its staged list
           auto test = [&](uint32_t w, uint32_t sl) { return table_probe<BW>(tab, (w << 5) | sl, G); };
-          hits += probe_lists(cols, pay, lane, bx, bl, slot, test);
+          hits += probe_lists<kP1Unified && !kBm>(cols, pay, lane, bx, bl, slot, test);
           continue_run(test);
         }
       }
