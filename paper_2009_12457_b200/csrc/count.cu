@@ -74,15 +74,6 @@ __device__ __forceinline__ T ld_stream(const T* p) {
   return *p;
 #endif
 }
-#ifndef BBTC_P1_DEPTH
-#define BBTC_P1_DEPTH 4   // A/B: 8 = rounds of eight 32-word loads in flight for long probe lists
-#endif
-#ifndef BBTC_DENSE_LIVE
-// A/B: the bit-row kernel skips the loads past a row's live uint4 (|V_k| bits of a
-// power-of-two stride): measured slower (rmat24 p=10 bit-row kernel 11.44 -> 12.18 ms,
-// orkut 1.15 -> 1.26; profiles/r02/r02u), so the full stride is loaded.
-#define BBTC_DENSE_LIVE 0
-#endif
 #ifndef BBTC_DEBUG_BOUNDS
 #define BBTC_DEBUG_BOUNDS 0   // debug builds: bounds checks in the list kernel (report via mapped host memory)
 #endif
@@ -109,12 +100,6 @@ __device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long lon
 #define BBTC_P1_UNIFIED 1   // phase 1: the last < 4 rounds of a long list in one predicated round
 #endif
 constexpr bool kP1Unified = BBTC_P1_UNIFIED;
-#ifndef BBTC_PF_NEXT
-#define BBTC_PF_NEXT 0   // A/B: rolling L2 prefetch of the next long probe list and of the remainders
-#endif
-#ifndef BBTC_TAIL3
-#define BBTC_TAIL3 0   // A/B: the last < 4 rounds of a long probe list with all loads in flight
-#endif
 #ifndef BBTC_LANEWALK_K
 #define BBTC_LANEWALK_K 2  // lane walk when 32 * max remainder <= K * sum of remainders + 64
 #endif
@@ -263,68 +248,32 @@ __device__ __forceinline__ uint32_t probe_lists(const uint32_t* __restrict__ col
   DBG_CHECK((unsigned long long)bx + bl <= g_dbg[8], 3, bx, bl, slot, g_dbg[8], 0, 0, 0);
 #endif
   uint32_t longs = __ballot_sync(kFull, bl >= 32);
-#if BBTC_PF_NEXT
-  // Rolling L2 prefetch: every lane asks for its own < 32-word remainder now (phase 2
-  // reads it after all long lists), and the lines of the next long list are requested
-  // while the current one is walked, so each list's first round finds it in L2.
-  if (bl & 31u) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + bx + (bl & ~31u)));
-  if (longs) {
-    const int s0 = __ffs(longs) - 1;
-    const uint32_t n0 = __shfl_sync(kFull, bl, s0), x0 = __shfl_sync(kFull, bx, s0);
-    if (32 * lane < n0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + x0 + 32 * lane));
-  }
-#endif
   while (longs) {
     const int src = __ffs(longs) - 1;
     longs &= longs - 1;
-#if BBTC_PF_NEXT
-    if (longs) {
-      const int s1 = __ffs(longs) - 1;
-      const uint32_t n1 = __shfl_sync(kFull, bl, s1), x1 = __shfl_sync(kFull, bx, s1);
-      if (32 * lane < n1) asm volatile("prefetch.global.L2 [%0];" ::"l"(cols + x1 + 32 * lane));
-    }
-#endif
     const uint32_t* B = cols + __shfl_sync(kFull, bx, src) + lane;
     const uint32_t nfull = __shfl_sync(kFull, bl, src) & ~31u;
     const uint32_t sl = __shfl_sync(kFull, slot, src);
     uint32_t off = 0;
-#if BBTC_P1_DEPTH == 8
-    for (; off + 256 <= nfull; off += 256) {
-      uint32_t w[8];
-#pragma unroll
-      for (int x = 0; x < 8; ++x) w[x] = B[off + 32 * x];
-#pragma unroll
-      for (int x = 0; x < 8; ++x) hits += test(w[x], sl);
-    }
-#endif
     // kUnified: rounds of up to four 32-word loads in flight, the last one predicated —
     // a list of 32-127 words costs one load latency instead of one per round.  In the
     // hash-only kernel variant (friendster 336.4 -> 331.4 ms); the bitmap variant, tighter
     // on registers, measured slower with it (rmat24 31.9 -> 32.2, orkut 11.89 -> 12.11;
     // profiles/r02/r02w).
     if constexpr (kUnified) {
-    for (; off < nfull; off += 128) {
-      const bool h2 = off + 32 < nfull, h3 = off + 64 < nfull, h4 = off + 96 < nfull;
-      const uint32_t w1 = B[off], w2 = h2 ? B[off + 32] : 0u, w3 = h3 ? B[off + 64] : 0u, w4 = h4 ? B[off + 96] : 0u;
-      hits += test(w1, sl) + (h2 ? test(w2, sl) : 0u) + (h3 ? test(w3, sl) : 0u) + (h4 ? test(w4, sl) : 0u);
-    }
+      for (; off < nfull; off += 128) {
+        const bool h2 = off + 32 < nfull, h3 = off + 64 < nfull, h4 = off + 96 < nfull;
+        const uint32_t w1 = B[off], w2 = h2 ? B[off + 32] : 0u, w3 = h3 ? B[off + 64] : 0u;
+        const uint32_t w4 = h4 ? B[off + 96] : 0u;
+        hits += test(w1, sl) + (h2 ? test(w2, sl) : 0u) + (h3 ? test(w3, sl) : 0u) + (h4 ? test(w4, sl) : 0u);
+      }
     } else {
-    for (; off + 128 <= nfull; off += 128) {
-      const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
-      hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
+      for (; off + 128 <= nfull; off += 128) {
+        const uint32_t w1 = B[off], w2 = B[off + 32], w3 = B[off + 64], w4 = B[off + 96];
+        hits += test(w1, sl) + test(w2, sl) + test(w3, sl) + test(w4, sl);
+      }
+      for (; off < nfull; off += 32) hits += test(B[off], sl);
     }
-    }
-#if BBTC_TAIL3
-    // the last 0-3 full rounds with their loads issued together (lists of 32-127 words
-    // otherwise wait out one load latency per round)
-    const uint32_t nr = (nfull - off) >> 5;
-    const uint32_t t1 = nr > 0 ? B[off] : 0u, t2 = nr > 1 ? B[off + 32] : 0u, t3 = nr > 2 ? B[off + 64] : 0u;
-    if (nr > 0) hits += test(t1, sl);
-    if (nr > 1) hits += test(t2, sl);
-    if (nr > 2) hits += test(t3, sl);
-#else
-    for (; off < nfull; off += 32) hits += test(B[off], sl);
-#endif
   }
   const uint32_t rem = bl & 31u;
 #if BBTC_LANEWALK
@@ -756,9 +705,7 @@ __global__ void k_dense_rows(const uint32_t* __restrict__ it_u, const uint32_t* 
 template <int S, bool kKeepU>
 __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it_v,
                                                 const uint32_t* __restrict__ Dik, const uint32_t* __restrict__ Djk,
-                                                uint64_t e_begin, uint64_t e_end, int lane, uint32_t live) {
-  // live = uint4 of a row that hold bits of V_k (ceil(|V_k| / 128)); the stride S is the
-  // next power of two: loads past the live part are skipped (they only read zeros).
+                                                uint64_t e_begin, uint64_t e_end, int lane) {
   constexpr int kV = S / 4;                      // uint4 per row
   constexpr int LPR = kV < 32 ? kV : 32;         // lanes per edge
   constexpr int Q = kV / LPR;                    // uint4 per lane per row
@@ -789,7 +736,7 @@ __device__ __forceinline__ uint32_t dense_edges(const uint32_t* __restrict__ it_
         const bool fresh = !kKeepU || uu != ku;
 #pragma unroll
         for (int x = 0; x < Q; ++x) {
-          if (idx < n && (uint32_t)(q + x * LPR) < live) {
+          if (idx < n) {
             a[r][x] = fresh ? Di[(uint64_t)uu * kV + x * LPR] : ka[x];
             b[r][x] = Dj[(uint64_t)vv * kV + x * LPR];
           } else {
@@ -847,15 +794,14 @@ k_count_dense(const uint32_t* __restrict__ it_u, const uint32_t* __restrict__ it
     const uint64_t e_begin = Bij.e0 + (g - item_start[lo]) * T.chunk;
     const uint64_t e_end = min(e_begin + T.chunk, Bij.e0 + Bij.nnz);
     uint32_t acc = 0;
-    const uint32_t live = BBTC_DENSE_LIVE ? (blocks[T.jk].nc + 127) / 128 : 0xFFFFFFFFu;   // |V_k| = columns of G_jk
     switch (T.pad) {
-      case 8: acc = dense_edges<8, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      case 16: acc = dense_edges<16, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      case 32: acc = dense_edges<32, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      case 64: acc = dense_edges<64, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      case 128: acc = dense_edges<128, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      case 256: acc = dense_edges<256, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
-      default: acc = dense_edges<512, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane, live); break;
+      case 8: acc = dense_edges<8, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 16: acc = dense_edges<16, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 32: acc = dense_edges<32, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 64: acc = dense_edges<64, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 128: acc = dense_edges<128, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      case 256: acc = dense_edges<256, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
+      default: acc = dense_edges<512, kKeepU>(it_u, it_v, Dik, Djk, e_begin, e_end, lane); break;
     }
     const uint32_t s = __reduce_add_sync(kFull, acc);
     if (lane == 0 && s) {
