@@ -170,7 +170,8 @@ BBTC_API bbtc_status bbtc_edges_map(const char* path, bbtc_edge_map* out);
 BBTC_API void bbtc_edges_unmap(bbtc_edge_map* m);
 /* bbtc_graph_from_edges for interleaved pairs (src0 dst0 src1 dst1 …, the binary edge
  * file layout) in host (mem = BBTC_MEM_HOST, pinned, pageable or memory-mapped) or device
- * memory.  Same result and errors as bbtc_graph_from_edges on the split arrays. */
+ * memory (device pairs 8-byte aligned, else BBTC_EINVAL).  Same result and errors as
+ * bbtc_graph_from_edges on the split arrays. */
 BBTC_API bbtc_status bbtc_graph_from_pairs(bbtc_ctx* ctx, const uint32_t* pairs, uint64_t n_edges, uint32_t n_hint,
                                            int mem, bbtc_graph** out);
 /* bbtc_edges_map + bbtc_graph_from_pairs(…, BBTC_MEM_HOST) + bbtc_edges_unmap: a graph

@@ -731,6 +731,8 @@ BBTC_API bbtc_status bbtc_graph_from_pairs(bbtc_ctx* ctx, const uint32_t* pairs,
     if (!ctx || !out) raise(BBTC_EINVAL, "ctx/out is NULL");
     *out = nullptr;
     if (n_edges && !pairs) raise(BBTC_EINVAL, "pairs is NULL");
+    if (mem == BBTC_MEM_DEVICE && (reinterpret_cast<uintptr_t>(pairs) & 7))
+      raise(BBTC_EINVAL, "device pairs must be 8-byte aligned (read as uint2)");
     if (mem != BBTC_MEM_HOST && mem != BBTC_MEM_DEVICE) raise(BBTC_EINVAL, "mem must be BBTC_MEM_HOST or _DEVICE");
     BBTC_CUDA(cudaSetDevice(ctx->device));
     auto* g = new bbtc_graph();
