@@ -96,9 +96,6 @@ __device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long lon
 #else
 #define DBG_CHECK(cond, code, a, b, c, d, e, f, g) do { } while (0)
 #endif
-#ifndef BBTC_EDGE_PF
-#define BBTC_EDGE_PF 0   // A/B: the next batch's edge ids loaded during this batch (hash-only variant)
-#endif
 #ifndef BBTC_P1_UNIFIED
 #define BBTC_P1_UNIFIED 1   // phase 1: the last < 4 rounds of a long list in one predicated round
 #endif
@@ -485,25 +482,14 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
 
     uint32_t hits = 0;
     uint64_t base = e_begin;
-    // kEdgePf: the next batch's edge ids are loaded as soon as this batch's length L is
-    // known, so they arrive while this batch stages and probes (a continued run moves
-    // the next batch's start; then they are loaded again).
-    constexpr bool kEdgePf = BBTC_EDGE_PF && !kBm && !kCP;
-    uint64_t pf_base = ~0ull;
-    uint32_t u_pf = 0, v_pf = 0;
     while (base < e_end) {
       // ---- 32 edges (u,v) of G_ij; key = the staged side's row (v by column, u by row)
       const uint64_t e = base + lane;
       const bool valid = e < e_end;
-      uint32_t u, v;
-      if (kEdgePf && base == pf_base) {
-        u = u_pf;
-        v = v_pf;
-      } else {
-        u = valid ? ld_stream(it_u + e) : 0xFFFFFFFFu;
-        if (cpm) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
-        else v = valid ? ld_stream(it_v + e) : 0xFFFFFFFFu;
-      }
+      const uint32_t u = valid ? ld_stream(it_u + e) : 0xFFFFFFFFu;
+      uint32_t v;
+      if (cpm) v = col_of(cpb, Bij.nc, ccol, (uint32_t)(e - Bij.e0), valid, lane);
+      else v = valid ? ld_stream(it_v + e) : 0xFFFFFFFFu;
       const uint32_t key = kCol ? v : u;
       const uint32_t pid = kCol ? u : v;
       uint32_t a0 = 0, alen = 0, bx = 0, blen = 0;   // a: staged list, b: probe list (bx: index in cols)
@@ -545,12 +531,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         else longl = true;
       }
       const bool in = lane < L;
-      if constexpr (kEdgePf) {
-        pf_base = base + L;
-        const uint64_t en = pf_base + lane;
-        u_pf = en < e_end ? ld_stream(it_u + en) : 0xFFFFFFFFu;
-        v_pf = en < e_end ? ld_stream(it_v + en) : 0xFFFFFFFFu;
-      }
       // edges whose staged list is empty cannot close a triangle: no probes for them
       const uint32_t bl = (in && alen > 0) ? blen : 0;
       // Ask L2 for every lane's probe list now (fire-and-forget, no registers): the
