@@ -144,7 +144,7 @@ def _run_shards(world, spec, p, host_input, backend="gloo"):
     return res
 
 
-@pytest.mark.parametrize("world,host_input", [(2, True), (3, False)])
+@pytest.mark.parametrize("world,host_input", [(2, True), (3, False), (5, True)])
 def test_sharded_build_matches_oracle(gpu, world, host_input):
     """§8(e): each rank holds 1/N of the raw edges (only that share crosses its PCIe link
     for host input), the sharded a1-a5 + block forwarding + a rank's own tasks, and one
