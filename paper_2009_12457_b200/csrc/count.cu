@@ -96,9 +96,6 @@ __device__ __noinline__ void dbg_fail(unsigned long long code, unsigned long lon
 #else
 #define DBG_CHECK(cond, code, a, b, c, d, e, f, g) do { } while (0)
 #endif
-#ifndef BBTC_PF_ROWS
-#define BBTC_PF_ROWS 0   // A/B: L2 prefetch of the next batch's row offsets (hash-only variant)
-#endif
 #ifndef BBTC_P1_UNIFIED
 #define BBTC_P1_UNIFIED 1   // phase 1: the last < 4 rounds of a long list in one predicated round
 #endif
@@ -534,27 +531,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
         else longl = true;
       }
       const bool in = lane < L;
-      // kPfRow: ask L2 for the next batch's edge ids now; after this batch's staging, read
-      // them (L2 hits by then) and ask L2 for their row offsets, so the next batch's first
-      // (random, dependent) gathers find them in L2 (no registers live across the batch).
-      constexpr bool kPfRow = BBTC_PF_ROWS && !kBm && !kCP;
-      if constexpr (kPfRow) {
-        const uint64_t en = base + L + lane;
-        if (en < e_end) {
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(it_u + en));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(it_v + en));
-        }
-      }
-      auto prefetch_next_rows = [&]() {
-        if constexpr (kPfRow) {
-          const uint64_t en = base + L + lane;
-          if (en < e_end) {
-            const uint32_t un = it_u[en], vn = it_v[en];
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rpS + (kCol ? vn : un)));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rpP + (kCol ? un : vn)));
-          }
-        }
-      };
       // edges whose staged list is empty cannot close a triangle: no probes for them
       const uint32_t bl = (in && alen > 0) ? blen : 0;
       // Ask L2 for every lane's probe list now (fire-and-forget, no registers): the
@@ -675,7 +651,6 @@ k_count(const uint32_t* __restrict__ cols, const uint32_t* __restrict__ it_u, co
                     return ld_stream(cS + P.x + f);
                   },
                   [&](uint32_t, uint2 P, uint32_t w) { table_insert<BW>(tab, (w << 5) | P.y, G); });
-          prefetch_next_rows();
           // ---- probe every word of each lane's list P against its staged list
           auto test = [&](uint32_t w, uint32_t sl) { return table_probe<BW>(tab, (w << 5) | sl, G); };
           hits += probe_lists<kP1Unified && !kBm>(cols, pay, lane, bx, bl, slot, test);
