@@ -621,7 +621,10 @@ def main():
                      "note": "physical: achieved = ncu DRAM bytes (read+write) per launch, measured in this run, "
                              "/ the launch's CUDA-event time; compulsory_frac = distinct bytes the kernel must read "
                              "/ time / peak; b_alg_logical_frac = SURVEY 8(d) B_alg / time / peak (logical, can "
-                             "exceed 1)."},
+                             "exceed 1); kernels.*.issue = warp instructions per launch / its event time vs SMs x 4 "
+                             "schedulers x the sampled SM clock, ncu_l1tex_pct / ncu_l2_pct = ncu throughput "
+                             "fractions of the same launch: the list kernel's limits where L2 serves most sectors "
+                             "(DESIGN 8)."},
         "clocks": clk.summary(),
         "triangles": tot,
         "paper_split": {
