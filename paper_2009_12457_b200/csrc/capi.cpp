@@ -379,6 +379,26 @@ void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32
     return r ? (double)bnnz[block_id(i, j)] / (double)r : 0.0;
   };
   auto bbytes = [&](uint32_t b, uint32_t i) { return 12.0 * (double)bnnz[b] + 4.0 * (double)(rows(i) + 1); };
+  // LPT weight = the task's measured-cost model, fitted to per-task device times
+  // (bbtc_task_times at the bench configs, profiles/r02/r02cc; scripts/balance_study.py):
+  //   list tasks  nnz(G_ij)·(16 + δ(G_ik)) + 2·min(nnz(G_ij), |V_j|)·δ(G_jk)
+  //   bit rows    0.145·nnz(G_ij)·(S + 35), S = the bit-row stride in words (plan_tasks'
+  //               isDense with the default dense bits and ratio)
+  // log-spread of time / estimate over rmat24 p=10's list tasks 0.50 -> 0.23, orkut p=8's
+  // 0.18 -> 0.15; the work-item estimate (edge_cost) overrated the bit-row tasks ~7x and
+  // the per-edge overhead of short probe lists ~2.7x, which left ranks 2x apart at N = 4-8.
+  static const uint32_t dense_bits = [] {
+    const char* e = getenv("BBTC_DENSE_BITS");
+    return std::min(e ? (uint32_t)atoi(e) : kDenseBitsDefault, kDenseMaxS * 32);
+  }();
+  static const double dense_ratio = getenv("BBTC_DENSE_RATIO") ? atof(getenv("BBTC_DENSE_RATIO")) : 4.0;
+  auto dense_stride = [&](uint32_t k) -> uint32_t {
+    const uint64_t vk = rows(k);
+    if (!vk || vk > dense_bits) return 0;
+    uint32_t s = kDenseMinS;
+    while ((uint64_t)s * 32 < vk) s <<= 1;
+    return s <= kDenseMaxS ? s : 0;
+  };
   struct T { double w; uint64_t idx; uint32_t i, j, k; };
   std::vector<T> ts;
   ts.reserve(nt);
@@ -386,8 +406,11 @@ void shard_assign(uint32_t p, const uint32_t* cuts, const uint64_t* bnnz, uint32
   for (uint32_t i = 0; i < p; ++i)
     for (uint32_t j = i; j < p; ++j)
       for (uint32_t k = j; k < p; ++k) {
-        const double w = (double)bnnz[block_id(i, j)] *
-                         edge_cost(delta(i, k), delta(j, k), (double)bnnz[block_id(i, j)], (double)rows(j));
+        const uint32_t S = dense_stride(k);
+        const bool dense = S && bnnz[block_id(i, j)] && delta(i, k) >= dense_ratio * S / 32.0;
+        const double nij = (double)bnnz[block_id(i, j)];
+        const double w = dense ? 0.145 * nij * (S + 35.0)
+                               : nij * (16.0 + delta(i, k)) + 2.0 * std::min(nij, (double)rows(j)) * delta(j, k);
         ts.push_back({w, task_index(p, i, j, k), i, j, k});
         total += w;
       }

@@ -30,16 +30,29 @@ def _random_blocks(rng, p, n=10000):
 
 
 def _work(p, cuts, bnnz):
-    """The scheduler's documented per-edge cost (capi.cpp edge_cost):
-    4 + δ(G_ik) + min(1, |V_j| / nnz_ij)·δ(G_jk) per edge of G_ij."""
+    """The scheduler's documented LPT weight (capi.cpp shard_assign): a
+    task counted through bit rows (isDense with the default 8192 dense bits and ratio 4:
+    bit-row stride S = the power of two >= |V_k| / 32 in [8, 512], δ(G_ik) >= 4·S/32)
+    weighs 0.145·nnz(G_ij)·(S + 35); any other nnz(G_ij)·(16 + δ(G_ik)) +
+    2·min(nnz(G_ij), |V_j|)·δ(G_jk)."""
     rows = np.diff(cuts.astype(np.float64))
     bid = lambda i, j: j * (j + 1) // 2 + i  # noqa: E731
     d = lambda i, j: bnnz[bid(i, j)] / rows[i] if rows[i] else 0.0  # noqa: E731
 
+    def stride(k):
+        if rows[k] == 0 or rows[k] > 8192:
+            return 0
+        s = 8
+        while s * 32 < rows[k]:
+            s *= 2
+        return s if s <= 512 else 0
+
     def cost(i, j, k):
         nij = float(bnnz[bid(i, j)])
-        run = min(1.0, rows[j] / nij) if nij > 0 else 1.0
-        return nij * (4 + d(i, k) + run * d(j, k))
+        S = stride(k)
+        if S and nij > 0 and d(i, k) >= 4 * S / 32:
+            return 0.145 * nij * (S + 35)
+        return nij * (16 + d(i, k)) + 2 * min(nij, rows[j]) * d(j, k)
     return [cost(i, j, k) for i in range(p) for j in range(i, p) for k in range(j, p)]
 
 
