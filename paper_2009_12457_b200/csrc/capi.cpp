@@ -307,6 +307,8 @@ void plan_tasks(bbtc_plan* plan, uint32_t /*world*/) {
                                     (double)(plan->cuts[j + 1] - plan->cuts[j]));
         if (plan->tasks.size() >= plan->dense_task_lo) per_edge = std::max(per_edge, 2.0 + plan->dense_s[k] / 8.0);
         uint64_t chunk = (uint64_t)(item_work / per_edge);
+        static const double dense_chunk_x = getenv("BBTC_DENSE_CHUNK_X") ? atof(getenv("BBTC_DENSE_CHUNK_X")) : 1.0;
+        if (plan->tasks.size() >= plan->dense_task_lo) chunk = (uint64_t)(chunk * dense_chunk_x);   // (A/B knob)
         chunk = std::max<uint64_t>(64, std::min<uint64_t>(1u << 16, (chunk + 31) / 32 * 32));
         T.chunk = (uint32_t)chunk;
         plan->tasks.push_back(T);
