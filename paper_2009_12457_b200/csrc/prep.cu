@@ -2005,6 +2005,10 @@ void plan_build_shard(bbtc_ctx* ctx, const bbtc_graph* like, const uint64_t* oke
   for (auto& A : plan->edge_arenas()) {
     DevBuf<uint32_t> g;
     g.alloc(std::max<uint64_t>(mg, 1), ctx);
+    // Blocks this rank neither builds nor receives stay zero (valid empty-looking data):
+    // whole-plan passes such as the column offsets of bbtc_plan_to_host index by their
+    // contents, which must not be uninitialised memory.
+    BBTC_CUDA(cudaMemsetAsync(g.p, 0, std::max<uint64_t>(mg, 1) * 4, st));
     for (uint32_t b = 0; b < nb; ++b) {
       const BlockDesc& B = plan->blocks[b];
       if (B.nnz) BBTC_CUDA(cudaMemcpyAsync(g.p + e0g[b], A.dev->p + B.e0, B.nnz * 4, cudaMemcpyDeviceToDevice, st));
