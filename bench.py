@@ -262,6 +262,10 @@ def main_sharded(args, world, rank, local):
     from paper_2009_12457_b200.dist import build_sharded, count_owner_h2d, max_over_ranks, reduce_counts
     cfg = inputs.CONFIGS[args.config]
     p = args.p or cfg.p
+    # At least 8 tasks per rank (unless --p is given): friendster's p = 4 has 20 tasks, whose
+    # best split over 8 ranks is 1.42x the mean load (scripts/balance_study.py).
+    while not args.p and bb.n_tasks(p) < 8 * world:
+        p += 1
     a, b = cfg.shard(rank, world)
     E = b - a
     hs = torch.empty(max(E, 1), dtype=torch.int32, pin_memory=True)[:E]
