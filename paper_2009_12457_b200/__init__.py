@@ -50,6 +50,7 @@ class EdgeMap:
         self.n_edges = n
         self.pairs = (np.ctypeslib.as_array(self._m.pairs, shape=(n, 2)) if n
                       else np.empty((0, 2), np.uint32))
+        self.pairs.flags.writeable = False   # a PROT_READ mapping: writes would fault
 
     def close(self):
         if getattr(self, "_m", None) is not None and L is not None and L.lib is not None:
