@@ -987,14 +987,9 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
     ds.alloc(std::min(E, 2 * chunk) * (pairs ? 2 : 1), ctx);   // (interleaved pairs: 8 B each, in ds)
     if (!pairs) dd.alloc(std::min(E, 2 * chunk), ctx);
     cudaStream_t cs = ctx->copy_streams[0];
-    // A/B (BBTC_H2D_STREAMS=2): the second half of each chunk's bytes on a second copy
-    // stream (both copy engines at once).
-    static const bool two = getenv("BBTC_H2D_STREAMS") && atoi(getenv("BBTC_H2D_STREAMS")) > 1;
-    cudaStream_t cs2 = two && ctx->copy_streams.size() > 1 ? ctx->copy_streams[1] : cs;
-    cudaEvent_t ev_copied[2], ev_copied2[2], ev_used[2];
+    cudaEvent_t ev_copied[2], ev_used[2];
     for (int x = 0; x < 2; ++x) {
       BBTC_CUDA(cudaEventCreateWithFlags(&ev_copied[x], cudaEventDisableTiming));
-      BBTC_CUDA(cudaEventCreateWithFlags(&ev_copied2[x], cudaEventDisableTiming));
       BBTC_CUDA(cudaEventCreateWithFlags(&ev_used[x], cudaEventDisableTiming));
       BBTC_CUDA(cudaEventRecord(ev_used[x], st));
     }
@@ -1003,23 +998,14 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       const uint64_t len = std::min(chunk, E - c0);
       const int slot = it & 1;
       BBTC_CUDA(cudaStreamWaitEvent(cs, ev_used[slot], 0));
-      if (cs2 != cs) BBTC_CUDA(cudaStreamWaitEvent(cs2, ev_used[slot], 0));
       if (pairs) {
-        const uint64_t h = cs2 != cs ? len / 2 : len;
-        BBTC_CUDA(cudaMemcpyAsync(ds.p + 2 * slot * chunk, pairs + 2 * c0, h * 8, cudaMemcpyHostToDevice, cs));
-        if (h < len)
-          BBTC_CUDA(cudaMemcpyAsync(ds.p + 2 * slot * chunk + 2 * h, pairs + 2 * (c0 + h), (len - h) * 8,
-                                    cudaMemcpyHostToDevice, cs2));
+        BBTC_CUDA(cudaMemcpyAsync(ds.p + 2 * slot * chunk, pairs + 2 * c0, len * 8, cudaMemcpyHostToDevice, cs));
       } else {
         BBTC_CUDA(cudaMemcpyAsync(ds.p + slot * chunk, src + c0, len * 4, cudaMemcpyHostToDevice, cs));
-        BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs2));
+        BBTC_CUDA(cudaMemcpyAsync(dd.p + slot * chunk, dst + c0, len * 4, cudaMemcpyHostToDevice, cs));
       }
       BBTC_CUDA(cudaEventRecord(ev_copied[slot], cs));
       BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied[slot], 0));
-      if (cs2 != cs) {
-        BBTC_CUDA(cudaEventRecord(ev_copied2[slot], cs2));
-        BBTC_CUDA(cudaStreamWaitEvent(st, ev_copied2[slot], 0));
-      }
       if (pairs) launch_canon(ds.p + 2 * slot * chunk, nullptr, len, c0, width);
       else launch_canon(ds.p + slot * chunk, dd.p + slot * chunk, len, c0, width);
       BBTC_CUDA(cudaEventRecord(ev_used[slot], st));
@@ -1032,7 +1018,6 @@ void graph_build(bbtc_ctx* ctx, const uint32_t* src, const uint32_t* dst, uint64
       }
     }
     for (int x = 0; x < 2; ++x) {
-      cudaEventDestroy(ev_copied2[x]);
       cudaEventDestroy(ev_copied[x]);
       cudaEventDestroy(ev_used[x]);
     }
